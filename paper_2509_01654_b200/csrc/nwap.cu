@@ -1,0 +1,551 @@
+// nwap.cu -- C ABI (include/nwap.h) over the sm_100a kernels in nwap_kernels.cuh.
+//
+// Host-side responsibilities: own the device copy of the word store, choose the
+// kernel variant, enumerate work units, reset/read statistics, slab pipelining
+// for host destinations, equal-work shard bounds.  No CPU scoring path exists
+// here: every score is produced by a CUDA kernel or the call fails.
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/nwap.h"
+#include "nwap_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(NWAP_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+static_assert(sizeof(nwap_dev_stats) == sizeof(nwap_stats), "stats layouts must agree");
+static_assert(sizeof(nwap_tile_smem) <= 227 * 1024, "tile shared memory too large");
+
+}  // namespace
+
+struct nwap_ctx {
+    int device = 0;
+    int sm_count = 0;
+    int64_t n = 0;
+    int qmax = 0;          // longest word
+    int qpad = 0;          // stored row width (multiple of 16)
+    int match = 0, mismatch = 0, gap = 0;
+    int K = 0;             // similarity table size (max symbol + 1 unless overridden)
+    bool general = false;  // explicit similarity table installed
+    std::vector<uint8_t> h_lens;        // host copy for shard arithmetic
+    std::vector<int64_t> h_lenprefix;   // prefix sums of lengths (n+1)
+    uint8_t *d_ids = nullptr;
+    uint8_t *d_lens = nullptr;          // padded with zeros to a whole number of strips
+    int8_t *d_sim = nullptr;            // K x K
+    nwap_dev_stats *d_stats = nullptr;
+    unsigned long long *d_counter = nullptr;
+    // compaction scratch
+    long long *d_block_counts = nullptr;
+    int64_t block_counts_cap = 0;
+    long long *d_total = nullptr;
+    // host-destination pipeline
+    int8_t *d_slab[2] = {nullptr, nullptr};
+    int64_t slab_bytes = 0;
+    cudaStream_t s_compute = nullptr, s_copy = nullptr;
+    cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    int occ_tiles[4] = {0, 0, 0, 0};    // resident CTAs/SM per (flavor, qw) instantiation
+};
+
+namespace {
+
+typedef void (*tile_kernel_t)(const nwap_tile_params);
+
+tile_kernel_t tile_kernel(int flavor, int qw)
+{
+    if (flavor == 0) return qw == 4 ? k_score_tiles<0, 4> : k_score_tiles<0, 8>;
+    return qw == 4 ? k_score_tiles<1, 4> : k_score_tiles<1, 8>;
+}
+
+int build_sim_table(nwap_ctx *c, const int8_t *sim_host)
+{
+    if (c->d_sim) { cudaFree(c->d_sim); c->d_sim = nullptr; }
+    CK(cudaMalloc(&c->d_sim, (size_t)c->K * c->K));
+    CK(cudaMemcpy(c->d_sim, sim_host, (size_t)c->K * c->K, cudaMemcpyHostToDevice));
+    return NWAP_OK;
+}
+
+int reset_stats(nwap_ctx *c, cudaStream_t st)
+{
+    k_init_stats<<<1, 256, 0, st>>>(c->d_stats, c->d_counter);
+    g_launches++;
+    CK(cudaGetLastError());
+    return NWAP_OK;
+}
+
+int fetch_stats(nwap_ctx *c, nwap_stats *out, cudaStream_t st)
+{
+    CK(cudaMemcpyAsync(out, c->d_stats, sizeof(nwap_stats), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return NWAP_OK;
+}
+
+void merge_stats(nwap_stats *acc, const nwap_stats *s, int want_hist)
+{
+    acc->sum += s->sum;
+    acc->count += s->count;
+    acc->min = std::min(acc->min, s->min);
+    acc->max = std::max(acc->max, s->max);
+    if (want_hist)
+        for (int b = 0; b < 256; ++b) acc->hist[b] += s->hist[b];
+}
+
+// Enqueue the scoring of [start, end) into out_dev on `st`.  Statistics accumulate
+// into c->d_stats (caller resets).  No synchronisation.
+int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int want_hist,
+                  int variant, cudaStream_t st)
+{
+    if (start >= end) return NWAP_OK;
+    const bool fast_ok = !c->general && c->qmax <= NWAP_MAXLEN_FAST;
+    if (variant == NWAP_VARIANT_AUTO) variant = fast_ok ? NWAP_VARIANT_PACKED : NWAP_VARIANT_SIMPLE;
+    if ((variant == NWAP_VARIANT_PACKED || variant == NWAP_VARIANT_PACKED3) && !fast_ok)
+        return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme and max word length <= %d (have %d%s)",
+                    NWAP_MAXLEN_FAST, c->qmax, c->general ? ", explicit similarity table" : "");
+
+    if (variant == NWAP_VARIANT_SIMPLE) {
+        nwap_simple_params p;
+        p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad; p.qmax = c->qmax;
+        p.start = start; p.end = end; p.out = out_dev; p.sim = c->d_sim; p.K = c->K; p.gap = c->gap;
+        p.stats = c->d_stats; p.want_hist = want_hist;
+        const size_t smem = (size_t)((c->K * c->K + 15) & ~15) + (size_t)(c->qmax + 1) * NWAP_SIMPLE_THREADS * sizeof(short);
+        CK(cudaFuncSetAttribute(k_score_simple, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int64_t pairs = end - start;
+        int64_t blocks = (pairs + NWAP_SIMPLE_THREADS - 1) / NWAP_SIMPLE_THREADS;
+        blocks = std::min<int64_t>(blocks, (int64_t)c->sm_count * 16);
+        k_score_simple<<<(unsigned)blocks, NWAP_SIMPLE_THREADS, smem, st>>>(p);
+        g_launches++;
+        CK(cudaGetLastError());
+        return NWAP_OK;
+    }
+
+    const int flavor = variant == NWAP_VARIANT_PACKED3 ? 1 : 0;
+    const int qw = c->qpad <= 16 ? 4 : 8;
+    nwap_tile_params p;
+    p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad;
+    p.start = start; p.end = end;
+    p.r_first = nwap_row_of(start, c->n);
+    p.c_start = nwap_col_of(start, c->n, p.r_first);
+    p.r_last = nwap_row_of(end - 1, c->n);
+    p.c_end = nwap_col_of(end - 1, c->n, p.r_last);
+    p.out = out_dev;
+    p.sc = nwap_make_consts(c->match, c->mismatch, c->gap);
+    p.stats = c->d_stats; p.want_hist = want_hist;
+    p.unit_counter = c->d_counter;
+
+    const int occ = std::max(1, c->occ_tiles[flavor * 2 + (qw == 8 ? 1 : 0)]);
+    const int64_t slots = (int64_t)c->sm_count * occ;
+    // bands per group: as large as possible (amortises the per-unit sort) while
+    // leaving >= 24 units per resident CTA for dynamic balance.
+    const int bands_per_strip = NWAP_C / NWAP_R;
+    int gb = 16;
+    nwap_unit_space us;
+    int64_t ubeg = 0, ucount = 0;
+    for (;; gb >>= 1) {
+        us.n = c->n; us.S = (c->n + NWAP_C - 1) / NWAP_C; us.gb = gb; us.gpk = bands_per_strip / gb;
+        const int64_t rows_per_group = (int64_t)gb * NWAP_R;
+        const int64_t g0 = p.r_first / rows_per_group, g1 = p.r_last / rows_per_group;
+        ubeg = nwap_units_before_group(us, g0);
+        ucount = nwap_units_before_group(us, g1 + 1) - ubeg;
+        if (gb == 1 || ucount >= slots * 24) break;
+    }
+    p.us = us; p.unit_begin = ubeg; p.unit_count = ucount;
+    const int64_t grid = std::min<int64_t>(slots, ucount);
+    CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
+    tile_kernel(flavor, qw)<<<(unsigned)grid, NWAP_THREADS, sizeof(nwap_tile_smem), st>>>(p);
+    g_launches++;
+    CK(cudaGetLastError());
+    return NWAP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *nwap_version(void) { return "nwap 0.1 (sm_100a)"; }
+const char *nwap_last_error(void) { return g_err.c_str(); }
+int64_t nwap_launch_count(void) { return g_launches.load(); }
+
+int nwap_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return fail(NWAP_ECUDA, "cudaGetDeviceCount failed"); }
+    return n;
+}
+
+int nwap_preflight(const uint8_t *lengths, int64_t n, int gap, int min_sim, int max_sim,
+                   int64_t *lo_out, int64_t *hi_out)
+{
+    if (n <= 0 || !lengths) return fail(NWAP_EINVAL, "word list is empty");
+    int64_t q = 0;
+    for (int64_t i = 0; i < n; ++i) q = std::max<int64_t>(q, lengths[i]);
+    const int64_t lo = std::min<int64_t>({0, 2 * q * gap, q * min_sim});
+    const int64_t hi = std::max<int64_t>({0, 2 * q * gap, q * max_sim});
+    if (lo_out) *lo_out = lo;
+    if (hi_out) *hi_out = hi;
+    if (lo < -128 || hi > 127)
+        return fail(NWAP_ERANGE, "scores would overflow 8-bit storage for max word length %lld: bounds [%lld, %lld]",
+                    (long long)q, (long long)lo, (long long)hi);
+    return (int)q;
+}
+
+int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, int q_stride,
+                const uint8_t *lengths, int match, int mismatch, int gap)
+{
+    if (!ctx_out || !ids || !lengths) return fail(NWAP_EINVAL, "null argument");
+    if (n < 2) return fail(NWAP_EINVAL, "need at least two words");
+    if (q_stride < 1 || q_stride > 255) return fail(NWAP_EINVAL, "q_stride %d out of range [1, 255]", q_stride);
+    int q = nwap_preflight(lengths, n, gap, std::min(match, mismatch), std::max(match, mismatch), nullptr, nullptr);
+    if (q < 0) return q;
+    if (q > q_stride) return fail(NWAP_EINVAL, "a word length (%d) exceeds q_stride (%d)", q, q_stride);
+    int maxsym = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int len = lengths[i];
+        if (len < 1) return fail(NWAP_EINVAL, "word %lld is empty (length 0)", (long long)i);
+        for (int j = 0; j < len; ++j) maxsym = std::max<int>(maxsym, ids[i * q_stride + j]);
+    }
+    CK(cudaSetDevice(device));
+    nwap_ctx *c = new nwap_ctx();
+    c->device = device; c->n = n; c->qmax = q; c->qpad = ((q + 15) / 16) * 16;
+    c->match = match; c->mismatch = mismatch; c->gap = gap; c->K = maxsym + 1;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    c->sm_count = prop.multiProcessorCount;
+
+    c->h_lens.assign(lengths, lengths + n);
+    c->h_lenprefix.resize(n + 1);
+    c->h_lenprefix[0] = 0;
+    for (int64_t i = 0; i < n; ++i) c->h_lenprefix[i + 1] = c->h_lenprefix[i] + lengths[i];
+
+    // repack rows to qpad on the host, then one H2D copy
+    std::vector<uint8_t> packed((size_t)n * c->qpad, 0);
+    for (int64_t i = 0; i < n; ++i) memcpy(&packed[(size_t)i * c->qpad], ids + i * q_stride, lengths[i]);
+    const int64_t lens_pad = ((n + NWAP_C - 1) / NWAP_C) * NWAP_C + NWAP_C;
+    int rc = NWAP_OK;
+    auto guard = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess && rc == NWAP_OK) rc = fail(NWAP_ECUDA, "%s failed: %s", what, cudaGetErrorString(e));
+    };
+    guard(cudaMalloc(&c->d_ids, packed.size()), "cudaMalloc(ids)");
+    guard(cudaMalloc(&c->d_lens, lens_pad), "cudaMalloc(lens)");
+    guard(cudaMalloc(&c->d_stats, sizeof(nwap_dev_stats)), "cudaMalloc(stats)");
+    guard(cudaMalloc(&c->d_counter, sizeof(unsigned long long)), "cudaMalloc(counter)");
+    guard(cudaMalloc(&c->d_total, sizeof(long long)), "cudaMalloc(total)");
+    if (rc == NWAP_OK) {
+        guard(cudaMemcpy(c->d_ids, packed.data(), packed.size(), cudaMemcpyHostToDevice), "H2D ids");
+        guard(cudaMemset(c->d_lens, 0, lens_pad), "memset lens");
+        guard(cudaMemcpy(c->d_lens, lengths, n, cudaMemcpyHostToDevice), "H2D lens");
+    }
+    if (rc == NWAP_OK) {
+        // uniform-scheme similarity table (engine.py:110-112) for the generic kernel
+        std::vector<int8_t> sim((size_t)c->K * c->K, (int8_t)mismatch);
+        for (int k = 0; k < c->K; ++k) sim[(size_t)k * c->K + k] = (int8_t)match;
+        rc = build_sim_table(c, sim.data());
+    }
+    if (rc == NWAP_OK) {
+        for (int f = 0; f < 2 && rc == NWAP_OK; ++f)
+            for (int w = 0; w < 2 && rc == NWAP_OK; ++w) {
+                tile_kernel_t k = tile_kernel(f, w ? 8 : 4);
+                guard(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(nwap_tile_smem)), "cudaFuncSetAttribute");
+                int occ = 0;
+                guard(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, sizeof(nwap_tile_smem)), "occupancy query");
+                c->occ_tiles[f * 2 + w] = occ;
+            }
+    }
+    if (rc != NWAP_OK) { nwap_destroy(c); return rc; }
+    *ctx_out = c;
+    return NWAP_OK;
+}
+
+int nwap_set_similarity(nwap_ctx *c, const int8_t *sim, int K)
+{
+    if (!c || !sim) return fail(NWAP_EINVAL, "null argument");
+    if (K < c->K) return fail(NWAP_EINVAL, "similarity table K=%d smaller than max symbol + 1 = %d", K, c->K);
+    if (K > 256) return fail(NWAP_EINVAL, "similarity table K=%d exceeds 256", K);
+    int mn = 127, mx = -128;
+    for (int a = 0; a < K; ++a)
+        for (int b = 0; b < K; ++b) {
+            if (sim[a * K + b] != sim[b * K + a]) return fail(NWAP_EINVAL, "similarity table is not symmetric at (%d, %d)", a, b);
+            mn = std::min<int>(mn, sim[a * K + b]);
+            mx = std::max<int>(mx, sim[a * K + b]);
+        }
+    int q = nwap_preflight(c->h_lens.data(), c->n, c->gap, mn, mx, nullptr, nullptr);
+    if (q < 0) return q;
+    CK(cudaSetDevice(c->device));
+    c->K = K;
+    c->general = true;
+    return build_sim_table(c, sim);
+}
+
+void nwap_destroy(nwap_ctx *c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaFree(c->d_ids); cudaFree(c->d_lens); cudaFree(c->d_sim); cudaFree(c->d_stats);
+    cudaFree(c->d_counter); cudaFree(c->d_block_counts); cudaFree(c->d_total);
+    cudaFree(c->d_slab[0]); cudaFree(c->d_slab[1]);
+    for (int i = 0; i < 2; ++i) {
+        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+        if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+    }
+    if (c->s_compute) cudaStreamDestroy(c->s_compute);
+    if (c->s_copy) cudaStreamDestroy(c->s_copy);
+    delete c;
+}
+
+int64_t nwap_num_words(const nwap_ctx *c) { return c ? c->n : 0; }
+int64_t nwap_num_edges(const nwap_ctx *c) { return c ? c->n * (c->n - 1) / 2 : 0; }
+int nwap_max_len(const nwap_ctx *c) { return c ? c->qmax : 0; }
+
+// cells in rows [0, r) plus the first (c - r - 1) pairs of row r
+static int64_t cells_before(const nwap_ctx *c, int64_t idx)
+{
+    const int64_t n = c->n, P = n * (n - 1) / 2;
+    if (idx <= 0) return 0;
+    const std::vector<int64_t> &pre = c->h_lenprefix;
+    auto row_cells_before = [&](int64_t r) {   // work of rows < r, O(r): cached below
+        int64_t w = 0;
+        for (int64_t k = 0; k < r; ++k) w += (int64_t)c->h_lens[k] * (pre[n] - pre[k + 1]);
+        return w;
+    };
+    if (idx >= P) return row_cells_before(n - 1);
+    const int64_t r = nwap_row_of(idx, n);
+    const int64_t col = nwap_col_of(idx, n, r);
+    return row_cells_before(r) + (int64_t)c->h_lens[r] * (pre[col] - pre[r + 1]);
+}
+
+int64_t nwap_cells_in_range(const nwap_ctx *c, int64_t start, int64_t end)
+{
+    if (!c || start >= end) return 0;
+    return cells_before(c, end) - cells_before(c, start);
+}
+
+int nwap_score_range(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, nwap_stats *stats_host,
+                     int want_hist, int variant, void *stream)
+{
+    if (!c) return fail(NWAP_EINVAL, "null context");
+    const int64_t P = nwap_num_edges(c);
+    if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
+    if (start < end && !out_dev) return fail(NWAP_EINVAL, "null output buffer");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = reset_stats(c, st);
+    if (rc) return rc;
+    rc = enqueue_score(c, start, end, out_dev, want_hist, variant, st);
+    if (rc) return rc;
+    if (stats_host) return fetch_stats(c, stats_host, st);
+    return NWAP_OK;
+}
+
+int nwap_read_stats(nwap_ctx *c, nwap_stats *stats_host, void *stream)
+{
+    if (!c || !stats_host) return fail(NWAP_EINVAL, "null argument");
+    CK(cudaSetDevice(c->device));
+    return fetch_stats(c, stats_host, (cudaStream_t)stream);
+}
+
+int nwap_score_range_host(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_host, nwap_stats *stats_host,
+                          int want_hist, int variant)
+{
+    if (!c) return fail(NWAP_EINVAL, "null context");
+    const int64_t P = nwap_num_edges(c);
+    if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
+    if (start < end && !out_host) return fail(NWAP_EINVAL, "null output buffer");
+    CK(cudaSetDevice(c->device));
+    if (!c->s_compute) {
+        CK(cudaStreamCreateWithFlags(&c->s_compute, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
+        }
+    }
+    const int64_t total = end - start;
+    // slab: large enough to amortise launches, small enough that the first copy starts early
+    int64_t slab = std::max<int64_t>(int64_t(8) << 20, std::min<int64_t>(int64_t(256) << 20, (total + 7) / 8));
+    slab = (slab + 255) & ~int64_t(255);
+    if (c->slab_bytes < slab) {
+        for (int i = 0; i < 2; ++i) { cudaFree(c->d_slab[i]); c->d_slab[i] = nullptr; }
+        CK(cudaMalloc(&c->d_slab[0], slab));
+        CK(cudaMalloc(&c->d_slab[1], slab));
+        c->slab_bytes = slab;
+    }
+    int rc = reset_stats(c, c->s_compute);
+    if (rc) return rc;
+    int k = 0;
+    for (int64_t pos = start; pos < end; pos += slab, ++k) {
+        const int b = k & 1;
+        const int64_t e = std::min(end, pos + slab);
+        if (k >= 2) CK(cudaStreamWaitEvent(c->s_compute, c->ev_free[b], 0));
+        rc = enqueue_score(c, pos, e, c->d_slab[b], want_hist, variant, c->s_compute);
+        if (rc) return rc;
+        CK(cudaEventRecord(c->ev_done[b], c->s_compute));
+        CK(cudaStreamWaitEvent(c->s_copy, c->ev_done[b], 0));
+        CK(cudaMemcpyAsync(out_host + (pos - start), c->d_slab[b], (size_t)(e - pos), cudaMemcpyDeviceToHost, c->s_copy));
+        CK(cudaEventRecord(c->ev_free[b], c->s_copy));
+    }
+    CK(cudaStreamSynchronize(c->s_copy));
+    if (stats_host) return fetch_stats(c, stats_host, c->s_compute);
+    CK(cudaStreamSynchronize(c->s_compute));
+    return NWAP_OK;
+}
+
+int nwap_payload_stats(nwap_ctx *c, const int8_t *payload_dev, int64_t count, nwap_stats *stats_host, void *stream)
+{
+    if (!c || !stats_host) return fail(NWAP_EINVAL, "null argument");
+    if (count < 0 || (count > 0 && !payload_dev)) return fail(NWAP_EINVAL, "bad payload");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = reset_stats(c, st);
+    if (rc) return rc;
+    if (count > 0) {
+        int64_t blocks = std::min<int64_t>((count / 16 + 255) / 256 + 1, (int64_t)c->sm_count * 8);
+        k_payload_stats<<<(unsigned)blocks, 256, 0, st>>>(payload_dev, count, c->d_stats);
+        g_launches++;
+        CK(cudaGetLastError());
+    }
+    return fetch_stats(c, stats_host, st);
+}
+
+int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end, int threshold,
+                       int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
+                       int32_t *degree_dev, void *stream)
+{
+    if (!c || !count_host) return fail(NWAP_EINVAL, "null argument");
+    const int64_t P = nwap_num_edges(c);
+    if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
+    if (cap < 0 || (cap > 0 && (!idx_out_dev || !score_out_dev))) return fail(NWAP_EINVAL, "bad output buffers");
+    *count_host = 0;
+    const int64_t count = end - start;
+    if (count == 0) return NWAP_OK;
+    if (!payload_dev) return fail(NWAP_EINVAL, "null payload");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nblocks = (count + NWAP_CMP_BLOCK - 1) / NWAP_CMP_BLOCK;
+    if (nblocks > 0x7fffffffLL) return fail(NWAP_EINVAL, "range too large for one compaction call; split it");
+    if (c->block_counts_cap < nblocks) {
+        cudaFree(c->d_block_counts); c->d_block_counts = nullptr;
+        CK(cudaMalloc(&c->d_block_counts, sizeof(long long) * (size_t)nblocks));
+        c->block_counts_cap = nblocks;
+    }
+    k_compact_count<<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, threshold, c->d_block_counts);
+    k_compact_scan<<<1, 1024, 0, st>>>(c->d_block_counts, nblocks, c->d_total);
+    k_compact_write<<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, start, c->n, threshold,
+                                                                  c->d_block_counts, idx_out_dev, score_out_dev, cap,
+                                                                  degree_dev);
+    g_launches += 3;
+    CK(cudaGetLastError());
+    long long total = 0;
+    CK(cudaMemcpyAsync(&total, c->d_total, sizeof total, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *count_host = total;
+    if (total > cap) return fail(NWAP_ECAPACITY, "compaction kept %lld edges but capacity is %lld", total, (long long)cap);
+    return NWAP_OK;
+}
+
+int nwap_equal_work_bounds(const nwap_ctx *c, int parts, int64_t *bounds_out)
+{
+    if (!c || !bounds_out || parts < 1) return fail(NWAP_EINVAL, "bad argument");
+    const int64_t n = c->n, P = n * (n - 1) / 2;
+    const std::vector<int64_t> &pre = c->h_lenprefix;
+    // rowpref[r] = cells in rows < r
+    std::vector<int64_t> rowpref(n + 1, 0);
+    for (int64_t r = 0; r < n; ++r) rowpref[r + 1] = rowpref[r] + (int64_t)c->h_lens[r] * (pre[n] - pre[r + 1]);
+    const __int128 W = rowpref[n];
+    bounds_out[0] = 0;
+    for (int g = 1; g < parts; ++g) {
+        const int64_t target = (int64_t)((W * g + parts - 1) / parts);
+        // first row r with rowpref[r+1] >= target
+        int64_t r = std::lower_bound(rowpref.begin() + 1, rowpref.end(), target) - (rowpref.begin() + 1);
+        r = std::min<int64_t>(r, n - 2);
+        const int64_t need = target - rowpref[r];
+        int64_t col = r + 1;
+        if (need > 0) {
+            const int64_t lr = c->h_lens[r];
+            const int64_t k = (need + lr - 1) / lr;
+            col = std::lower_bound(pre.begin(), pre.end(), pre[r + 1] + k) - pre.begin();
+        }
+        int64_t idx = nwap_before_row(r, n) + (col - r - 1);
+        idx = std::min(std::max(idx, bounds_out[g - 1]), P);
+        bounds_out[g] = idx;
+    }
+    bounds_out[parts] = P;
+    return NWAP_OK;
+}
+
+int nwap_rows_cols(int64_t n, const int64_t *idx_dev, int64_t count, int64_t *rows_dev, int64_t *cols_dev, void *stream)
+{
+    if (n < 2 || count < 0) return fail(NWAP_EINVAL, "bad argument");
+    if (count == 0) return NWAP_OK;
+    const int64_t blocks = std::min<int64_t>((count + 255) / 256, 4096);
+    k_rows_cols<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(n, idx_dev, count, rows_dev, cols_dev);
+    g_launches++;
+    CK(cudaGetLastError());
+    return NWAP_OK;
+}
+
+int nwap_probe(int device, int which, int iters, double *ipc_out, double *ms_out)
+{
+    if (which < 0 || which >= NWAP_PROBE_COUNT || iters < 1 || !ipc_out || !ms_out) return fail(NWAP_EINVAL, "bad argument");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    const int blocks = prop.multiProcessorCount;
+    uint32_t *sink = nullptr;
+    long long *cycles = nullptr;
+    CK(cudaMalloc(&sink, 64));
+    CK(cudaMalloc(&cycles, sizeof(long long) * blocks));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    typedef void (*probe_t)(int, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t *, long long *);
+    static const probe_t table[NWAP_PROBE_COUNT] = {k_probe<0>, k_probe<1>, k_probe<2>, k_probe<3>,
+                                                    k_probe<4>, k_probe<5>, k_probe<6>, k_probe<7>};
+    for (int rep = 0; rep < 2; ++rep) {   // first launch warms up
+        CK(cudaEventRecord(e0));
+        table[which]<<<blocks, 512>>>(iters, 0x00030005u, 0xfffefffdu, 0x00070009u, 1u, sink, cycles);
+        CK(cudaEventRecord(e1));
+        g_launches++;
+        CK(cudaGetLastError());
+        CK(cudaEventSynchronize(e1));
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    std::vector<long long> h(blocks);
+    CK(cudaMemcpy(h.data(), cycles, sizeof(long long) * blocks, cudaMemcpyDeviceToHost));
+    long long mx = 1;
+    for (long long v : h) mx = std::max(mx, v);
+    const double per_thread = which >= 6 ? 4.0 : 1.0;      // instructions per chain step
+    const double warp_instr = (double)iters * 16 * 8 * per_thread * (512 / 32);
+    *ipc_out = warp_instr / (double)mx;
+    *ms_out = ms;
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    cudaFree(sink); cudaFree(cycles);
+    return NWAP_OK;
+}
+
+}  // extern "C"

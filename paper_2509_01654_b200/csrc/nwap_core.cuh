@@ -1,0 +1,176 @@
+// nwap_core.cuh -- the packed Needleman-Wunsch cell update (device + host emulation).
+//
+// Replaces the inner loops of reference engine.py:159-172 (_nw_batch) for the
+// uniform match/mismatch/gap scheme.  Two pairs -- (row word, column word 0) and
+// (row word, column word 1) -- live in the two 16-bit halves of every 32-bit
+// register ("s16x2").  The rolling score-matrix row stays in registers.
+//
+// Potential transform (exact integer algebra):
+//     H'[i][j] = H[i][j] - (match-gap)*i - gap*j + BIAS
+// turns   H[i][j] = max(H[i-1][j-1] + sim, H[i-1][j] + gap, H[i][j-1] + gap)
+// into    H'[i][j] = max(H'[i-1][j-1] - e*D,  H'[i-1][j] + u,  H'[i][j-1])
+// with e = [a_i != b_j] in {0,1}, D = match - mismatch, u = 2*gap - match,
+// boundary H'[0][j] = BIAS, H'[i][0] = BIAS + i*u.
+// Per packed cell (2 DP cells) that is
+//     e   = VIADDMNMX.U16x2 (a + (-b), min 1)        ALU pipe
+//     dw  = IMAD            (e * (-D) + diag)        FMA pipe  (packed-safe: halves stay in [0,2^15))
+//     cur = VIMNMX3.S16x2   (dw, up_plus_u, left)    ALU pipe
+//     upu = IMAD            (cur * 1 + u*65537)      FMA pipe  (next row's up + u)
+// i.e. 2 ALU + 2 FMA-pipe issues (FLAVOR 0).  FLAVOR 1 folds the vertical add
+// into VIADDMNMX.S16x2 instead (3 ALU + 1 IMAD, one rolling array).
+//
+// All halves stay inside [0, 2^15): |H| <= 128 by the int8 preflight
+// (engine.py:72-96), |(match-gap)*i| <= 192, |gap*j| <= 64, |D| <= 256, and
+// BIAS = 8192, so 32-bit IMAD never carries between halves and signed/unsigned
+// 16-bit max agree.
+#pragma once
+#include <stdint.h>
+#include "nwap_index.cuh"
+
+#define NWAP_BIAS 8192u
+#define NWAP_BIAS2 (NWAP_BIAS | (NWAP_BIAS << 16))
+
+struct nwap_scheme_consts {
+    uint32_t neg_delta;   // (uint32)(-(match - mismatch))            IMAD multiplier
+    uint32_t u2;          // (uint32)((2*gap - match) * 65537)        32-bit packed addend
+    uint32_t u2h;         // uint16(2*gap - match) replicated         per-half addend (VIADDMNMX)
+    uint32_t one;         // 1, opaque to the compiler so `cur*one+u2` stays an IMAD
+    int32_t alpha;        // match - gap   (row potential)
+    int32_t beta;         // gap           (column potential)
+};
+
+NWAP_HD nwap_scheme_consts nwap_make_consts(int match, int mismatch, int gap)
+{
+    nwap_scheme_consts c;
+    int u = 2 * gap - match;
+    c.neg_delta = (uint32_t)(-(match - mismatch));
+    c.u2 = (uint32_t)(u * 65537);
+    c.u2h = ((uint32_t)(uint16_t)(int16_t)u) * 0x10001u;
+    c.one = 1u;
+    c.alpha = match - gap;
+    c.beta = gap;
+    return c;
+}
+
+// ---- DPX intrinsics with host emulation ------------------------------------
+#if defined(__CUDA_ARCH__)
+#define NWAP_DEV_INTRIN 1
+#else
+#define NWAP_DEV_INTRIN 0
+#endif
+
+NWAP_HD uint32_t nwap_viaddmin_u16x2(uint32_t a, uint32_t b, uint32_t c)
+{
+#if NWAP_DEV_INTRIN
+    return __viaddmin_u16x2(a, b, c);
+#else
+    uint32_t lo = ((a & 0xffffu) + (b & 0xffffu)) & 0xffffu, hi = ((a >> 16) + (b >> 16)) & 0xffffu;
+    uint32_t cl = c & 0xffffu, ch = c >> 16;
+    return (lo < cl ? lo : cl) | ((hi < ch ? hi : ch) << 16);
+#endif
+}
+
+NWAP_HD uint32_t nwap_vimax3_s16x2(uint32_t a, uint32_t b, uint32_t c)
+{
+#if NWAP_DEV_INTRIN
+    return __vimax3_s16x2(a, b, c);
+#else
+    int16_t al = (int16_t)(a & 0xffffu), ah = (int16_t)(a >> 16);
+    int16_t bl = (int16_t)(b & 0xffffu), bh = (int16_t)(b >> 16);
+    int16_t cl = (int16_t)(c & 0xffffu), ch = (int16_t)(c >> 16);
+    int16_t ml = al > bl ? al : bl; ml = ml > cl ? ml : cl;
+    int16_t mh = ah > bh ? ah : bh; mh = mh > ch ? mh : ch;
+    return (uint32_t)(uint16_t)ml | ((uint32_t)(uint16_t)mh << 16);
+#endif
+}
+
+NWAP_HD uint32_t nwap_viaddmax_s16x2(uint32_t a, uint32_t b, uint32_t c)
+{
+#if NWAP_DEV_INTRIN
+    return __viaddmax_s16x2(a, b, c);
+#else
+    int16_t sl = (int16_t)(uint16_t)((a & 0xffffu) + (b & 0xffffu));
+    int16_t sh = (int16_t)(uint16_t)((a >> 16) + (b >> 16));
+    int16_t cl = (int16_t)(c & 0xffffu), ch = (int16_t)(c >> 16);
+    int16_t ml = sl > cl ? sl : cl, mh = sh > ch ? sh : ch;
+    return (uint32_t)(uint16_t)ml | ((uint32_t)(uint16_t)mh << 16);
+#endif
+}
+
+NWAP_HD uint32_t nwap_vmaxs2(uint32_t a, uint32_t b)
+{
+#if NWAP_DEV_INTRIN
+    return __vmaxs2(a, b);
+#else
+    return nwap_vimax3_s16x2(a, b, b);
+#endif
+}
+
+// Negated, packed column symbols: half 0 = -b0[j], half 1 = -b1[j] (mod 2^16),
+// so that (a*65537 + nb) has a zero half exactly where the symbols are equal.
+NWAP_HD uint32_t nwap_pack_negb(uint32_t b0, uint32_t b1)
+{
+    return ((0u - b0) & 0xffffu) | ((0u - b1) << 16);
+}
+
+// One score-matrix row (one symbol of the row word, packed as a*65537) against
+// the LB register-resident columns.  FIRST = this is matrix row 1, whose
+// "previous row" is the constant boundary, so P/PU are written, not read.
+// left0 is H'[i][0] for this row (both halves).
+template <int LB, int FLAVOR, bool FIRST>
+NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t (&nb)[LB], uint32_t (&P)[LB + 1],
+                         uint32_t (&PU)[LB + 1], uint32_t left0, const nwap_scheme_consts &sc)
+{
+    uint32_t diag = FIRST ? NWAP_BIAS2 : P[0];
+    P[0] = left0;
+    uint32_t left = left0;
+    const uint32_t bias_u2 = NWAP_BIAS2 + sc.u2;
+#pragma unroll
+    for (int j = 1; j <= LB; ++j) {
+        uint32_t e = nwap_viaddmin_u16x2(a2, nb[j - 1], 0x00010001u);
+        uint32_t dw = e * sc.neg_delta + diag;
+        uint32_t cur;
+        if (FLAVOR == 0) {
+            uint32_t upu = FIRST ? bias_u2 : PU[j];
+            diag = FIRST ? NWAP_BIAS2 : P[j];
+            cur = nwap_vimax3_s16x2(dw, upu, left);
+            PU[j] = cur * sc.one + sc.u2;
+        } else {
+            uint32_t up = FIRST ? NWAP_BIAS2 : P[j];
+            diag = up;
+            uint32_t t = nwap_viaddmax_s16x2(up, sc.u2h, dw);
+            cur = nwap_vmaxs2(t, left);
+        }
+        P[j] = cur;
+        left = cur;
+    }
+}
+
+// Whole pair-of-pairs DP for one row word; returns the packed H' values at
+// (la, lb0) in the low half and (la, lb1) in the high half.  Used by the host
+// emulation test and (unrolled differently) by the tile kernel.
+template <int LB, int FLAVOR>
+NWAP_HD uint32_t nwap_dp_pair(const uint32_t *row_sym2, int la, const uint32_t (&nb)[LB],
+                              int lb0, int lb1, const nwap_scheme_consts &sc)
+{
+    uint32_t P[LB + 1], PU[LB + 1];
+    uint32_t left0 = NWAP_BIAS2 + sc.u2;
+    nwap_dp_row<LB, FLAVOR, true>(row_sym2[0], nb, P, PU, left0, sc);
+    for (int i = 1; i < la; ++i) {
+        left0 += sc.u2;
+        nwap_dp_row<LB, FLAVOR, false>(row_sym2[i], nb, P, PU, left0, sc);
+    }
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int j = 1; j <= LB; ++j) {
+        if (j == lb0) lo = P[j] & 0xffffu;
+        if (j == lb1) hi = P[j] >> 16;
+    }
+    return lo | (hi << 16);
+}
+
+// H'[la][lb] (one half, biased) -> true score.
+NWAP_HD int nwap_unbias(uint32_t half, int la, int lb, const nwap_scheme_consts &sc)
+{
+    return (int)half - (int)NWAP_BIAS + sc.alpha * la + sc.beta * lb;
+}

@@ -1,0 +1,311 @@
+"""B200 scoring engine behind the reference's entry point.
+
+``compute_all_pairs(words, scheme, sink, plan) -> ComputeStats`` has the
+signature, return type, error behaviour and sink protocol of the reference's
+``phonsim.engine.compute_all_pairs`` (engine.py:218-290); ``NwapContext.score_range``
+is the ``_score_range`` seam (engine.py:176-195) with a device (or pinned host)
+destination.  All scoring happens in libnwap.so's CUDA kernels; torch is used
+only to own device / pinned buffers and the current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from ._native import NwapStats, VARIANTS, check, lib
+from .host_types import (ComputePlan, ComputeStats, DataError, ScoringScheme, same_scheme,
+                         scheme_fields)
+from .triangle import num_edges
+
+
+def preflight_range_check(words, scheme) -> int:
+    """Reference engine.py:72-96, same messages: returns q or raises."""
+    if not words:
+        raise ValueError("word list is empty")
+    q = max(len(w.phonemes) for w in words)
+    match, mismatch, gap, overrides = scheme_fields(scheme)
+    sims = [match, mismatch, *overrides.values()]
+    lo = min(0, 2 * q * gap, q * min(sims))
+    hi = max(0, 2 * q * gap, q * max(sims))
+    problems = []
+    if lo < -128:
+        problems.append(f"minimum achievable score {lo} < -128")
+    if hi > 127:
+        problems.append(f"maximum achievable score {hi} > 127")
+    if problems:
+        raise DataError("scores would overflow 8-bit storage for max word length "
+                        f"{q}: {'; '.join(problems)}")
+    return q
+
+
+def pack_words(words, q: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray]:
+    """Reference engine.py:99-107 with uint8 symbols: (n, q) ids + (n,) lengths."""
+    n = len(words)
+    lengths = np.fromiter((len(w.phonemes) for w in words), dtype=np.int64, count=n)
+    if q is None:
+        q = int(lengths.max())
+    if q > 255:
+        raise DataError(f"word length {q} exceeds the 255-symbol store limit")
+    if lengths.min() < 1:
+        raise ValueError(f"word {int(np.argmin(lengths))} has no phonemes")
+    ids = np.zeros((n, q), dtype=np.uint8)
+    for i, w in enumerate(words):
+        ph = w.phonemes
+        if ph and (max(ph) > 255 or min(ph) < 0):
+            raise DataError(f"word {i}: phoneme id outside [0, 255]")
+        ids[i, : len(ph)] = ph
+    return ids, lengths.astype(np.uint8)
+
+
+def similarity_table(scheme, size: int) -> np.ndarray:
+    """Reference engine.py:110-117 as int8."""
+    match, mismatch, _, overrides = scheme_fields(scheme)
+    sim = np.full((size, size), mismatch, dtype=np.int64)
+    np.fill_diagonal(sim, match)
+    for (a, b), v in overrides.items():
+        if a < size and b < size:
+            sim[a, b] = v
+            sim[b, a] = v
+    if sim.min() < -128 or sim.max() > 127:
+        raise DataError("similarity value does not fit int8")
+    return sim.astype(np.int8)
+
+
+def _stats_tuple(st: NwapStats, want_hist: bool):
+    hist = np.ctypeslib.as_array(st.hist).astype(np.int64).copy() if want_hist else None
+    return int(st.sum), int(st.min), int(st.max), int(st.count), hist
+
+
+class NwapContext:
+    """One word store resident on one GPU (nwap_ctx)."""
+
+    def __init__(self, ids: np.ndarray, lengths: np.ndarray, scheme, device: int = 0):
+        ids = np.ascontiguousarray(ids, dtype=np.uint8)
+        lengths = np.ascontiguousarray(lengths, dtype=np.uint8)
+        if ids.ndim != 2 or lengths.ndim != 1 or ids.shape[0] != lengths.shape[0]:
+            raise ValueError("ids must be (n, q) and lengths (n,)")
+        match, mismatch, gap, overrides = scheme_fields(scheme)
+        self.scheme = (match, mismatch, gap)
+        self.device = device
+        self.n = int(lengths.shape[0])
+        self._h = ctypes.c_void_p()
+        L = lib()
+        check(L.nwap_create(ctypes.addressof(self._h), device, ids.ctypes.data, self.n, ids.shape[1],
+                            lengths.ctypes.data, match, mismatch, gap))
+        if overrides:
+            size = int(ids.max()) + 1
+            sim = similarity_table(scheme, size)
+            try:
+                check(L.nwap_set_similarity(self._h, sim.ctypes.data, size))
+            except Exception:
+                self.close()
+                raise
+
+    @classmethod
+    def from_words(cls, words, scheme, device: int = 0) -> "NwapContext":
+        q = preflight_range_check(words, scheme)
+        ids, lengths = pack_words(words, q)
+        return cls(ids, lengths, scheme, device)
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().nwap_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- geometry
+    @property
+    def num_edges(self) -> int:
+        return int(lib().nwap_num_edges(self._h))
+
+    @property
+    def max_len(self) -> int:
+        return int(lib().nwap_max_len(self._h))
+
+    def cells_in_range(self, start: int, end: int) -> int:
+        return int(lib().nwap_cells_in_range(self._h, start, end))
+
+    def equal_work_bounds(self, parts: int) -> np.ndarray:
+        out = np.zeros(parts + 1, dtype=np.int64)
+        check(lib().nwap_equal_work_bounds(self._h, parts, out.ctypes.data))
+        return out
+
+    # -- scoring
+    def score_range(self, start: int, end: int, out, want_hist: bool = False, variant: str = "auto",
+                    sync: bool = True):
+        """Score edges [start, end) into ``out`` (torch int8/uint8 CUDA tensor, >= end-start
+        elements).  Returns (sum, min, max, count, hist|None); with sync=False returns None and
+        leaves the statistics on the device (read_stats())."""
+        import torch
+
+        if not (out.is_cuda and out.is_contiguous() and out.element_size() == 1):
+            raise ValueError("out must be a contiguous 1-byte CUDA tensor")
+        if out.numel() < end - start:
+            raise ValueError("output tensor too small")
+        stream = torch.cuda.current_stream(out.device).cuda_stream
+        st = NwapStats()
+        check(lib().nwap_score_range(self._h, start, end, out.data_ptr(),
+                                     ctypes.addressof(st) if sync else None, int(want_hist),
+                                     VARIANTS[variant], stream))
+        return _stats_tuple(st, want_hist) if sync else None
+
+    def read_stats(self, want_hist: bool = False):
+        import torch
+
+        st = NwapStats()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(lib().nwap_read_stats(self._h, ctypes.addressof(st), stream))
+        return _stats_tuple(st, want_hist)
+
+    def score_range_host(self, start: int, end: int, out_host, want_hist: bool = False,
+                         variant: str = "auto"):
+        """Same seam with a host destination (numpy uint8/int8 array or pinned torch tensor)."""
+        ptr, size = _host_ptr(out_host)
+        if size < end - start:
+            raise ValueError("output buffer too small")
+        st = NwapStats()
+        check(lib().nwap_score_range_host(self._h, start, end, ptr, ctypes.addressof(st),
+                                          int(want_hist), VARIANTS[variant]))
+        return _stats_tuple(st, want_hist)
+
+    def payload_stats(self, payload, count: Optional[int] = None):
+        import torch
+
+        count = payload.numel() if count is None else count
+        st = NwapStats()
+        stream = torch.cuda.current_stream(payload.device).cuda_stream
+        check(lib().nwap_payload_stats(self._h, payload.data_ptr(), count, ctypes.addressof(st), stream))
+        return _stats_tuple(st, True)
+
+    def compact_range(self, payload, start: int, end: int, threshold: int, capacity: int,
+                      degree=None):
+        """Kept edges (score >= threshold) of an already scored slice, in index order.
+        Returns (idx int64 tensor, score int8 tensor); ``degree`` (int32 CUDA tensor of n)
+        is incremented at both endpoints of every kept edge."""
+        import torch
+
+        dev = payload.device
+        idx = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
+        sc = torch.empty(max(capacity, 1), dtype=torch.int8, device=dev)
+        cnt = ctypes.c_int64()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = lib().nwap_compact_range(self._h, payload.data_ptr(), start, end, threshold,
+                                      idx.data_ptr(), sc.data_ptr(), capacity, ctypes.addressof(cnt),
+                                      degree.data_ptr() if degree is not None else None, stream)
+        if rc == _native.NWAP_ECAPACITY:
+            raise _native.CapacityError(_native.last_error(), cnt.value)
+        check(rc)
+        return idx[: cnt.value], sc[: cnt.value]
+
+
+def _host_ptr(buf):
+    if isinstance(buf, np.ndarray):
+        if not buf.flags["C_CONTIGUOUS"] or buf.itemsize != 1:
+            raise ValueError("host buffer must be a contiguous 1-byte array")
+        return buf.ctypes.data, buf.size
+    if hasattr(buf, "data_ptr"):
+        if buf.is_cuda or buf.element_size() != 1 or not buf.is_contiguous():
+            raise ValueError("host buffer must be a contiguous 1-byte CPU tensor")
+        return buf.data_ptr(), buf.numel()
+    raise TypeError("unsupported host buffer")
+
+
+def device_rows_cols(idx: "np.ndarray", n: int):
+    """triangle.py:93-112 on the device (parity tests)."""
+    import torch
+
+    t = torch.as_tensor(np.ascontiguousarray(idx, dtype=np.int64)).cuda()
+    rows = torch.empty_like(t)
+    cols = torch.empty_like(t)
+    check(lib().nwap_rows_cols(n, t.data_ptr(), t.numel(), rows.data_ptr(), cols.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return rows.cpu().numpy(), cols.cpu().numpy()
+
+
+def probe(which: str, iters: int = 2000, device: int = 0):
+    """(warp-instructions per SM per clock, milliseconds) of one issue probe."""
+    ipc = ctypes.c_double()
+    ms = ctypes.c_double()
+    check(lib().nwap_probe(device, _native.PROBES.index(which), iters, ctypes.addressof(ipc),
+                           ctypes.addressof(ms)))
+    return ipc.value, ms.value
+
+
+def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan] = None,
+                      device: int = 0, variant: str = "auto") -> ComputeStats:
+    """Drop-in for reference engine.py:218-290.
+
+    Every edge score goes through ``sink.write`` once, in linear-index order, in
+    pieces of ``plan.chunk_size`` edges (the payload never depends on it); on any
+    failure ``sink.abort()`` is called before the exception propagates.
+    """
+    import torch
+
+    n = len(words)
+    q = preflight_range_check(words, scheme)
+    if plan is None:
+        plan = ComputePlan(n=n, scheme=scheme)
+    if plan.n != n:
+        raise ValueError(f"plan is for n={plan.n}, got {n} words")
+    if not same_scheme(plan.scheme, scheme):
+        raise ValueError("plan scheme differs from the scheme argument")
+    if not torch.cuda.is_available():
+        raise RuntimeError("compute_all_pairs needs a CUDA device: there is no CPU fallback")
+
+    ids, lengths = pack_words(words, q)
+    total = num_edges(n)
+    edges = 0
+    score_sum = 0
+    score_min = 127
+    score_max = -128
+    started = time.perf_counter()
+    ctx = None
+    try:
+        ctx = NwapContext(ids, lengths, scheme, device)
+        chunk = plan.chunk_size
+        # host staging slab: a whole number of sink chunks, about 64 MiB
+        slab = max(chunk, ((64 << 20) // chunk) * chunk)
+        slab = min(slab, -(-total // chunk) * chunk)
+        staging = torch.empty(slab, dtype=torch.int8).pin_memory()
+        view = memoryview(staging.numpy()).cast("B")
+        for s in range(0, total, slab):
+            e = min(s + slab, total)
+            ssum, smin, smax, scount, _ = ctx.score_range_host(s, e, staging, variant=variant)
+            if scount != e - s:
+                raise DataError(f"device scored {scount} edges in [{s}, {e})")
+            for cs in range(0, e - s, chunk):
+                piece = view[cs: min(cs + chunk, e - s)]
+                sink.write(piece)
+                edges += len(piece)
+            score_sum += ssum
+            score_min = min(score_min, smin)
+            score_max = max(score_max, smax)
+    except Exception:
+        sink.abort()
+        raise
+    finally:
+        if ctx is not None:
+            ctx.close()
+    wall = time.perf_counter() - started
+    if edges != total:
+        sink.abort()
+        raise DataError(f"wrote {edges} edges, expected {total}")
+    return ComputeStats(edges_written=edges, wall_time=wall, min_score=score_min,
+                        max_score=score_max, mean_score=score_sum / edges)

@@ -1,0 +1,68 @@
+// tests/native/host_emul.cpp -- compiles the device headers as plain C++ so the
+// packed-recurrence algebra and the index/unit arithmetic can be checked on a
+// CPU against the oracle (tests/test_core_emul.py).  Test infrastructure only.
+#include <stdint.h>
+#include <string.h>
+#include "nwap_index.cuh"
+#include "nwap_core.cuh"
+
+template <int LB, int FLAVOR>
+static uint32_t run_pair(const uint8_t *a, int la, const uint8_t *b0, int lb0,
+                         const uint8_t *b1, int lb1, const nwap_scheme_consts &sc)
+{
+    uint32_t row2[256];
+    for (int i = 0; i < la; ++i) row2[i] = (uint32_t)a[i] * 65537u;
+    uint32_t nb[LB];
+    for (int j = 0; j < LB; ++j)
+        nb[j] = nwap_pack_negb(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
+    return nwap_dp_pair<LB, FLAVOR>(row2, la, nb, lb0, lb1, sc);
+}
+
+template <int FLAVOR>
+static uint32_t dispatch(int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0,
+                         const uint8_t *b1, int lb1, const nwap_scheme_consts &sc)
+{
+    switch (LB) {
+#define CASE(n) case n: return run_pair<n, FLAVOR>(a, la, b0, lb0, b1, lb1, sc);
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+        CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24)
+        CASE(25) CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
+#undef CASE
+    }
+    return 0;
+}
+
+extern "C" {
+
+// Scores (a vs b0) and (a vs b1) with the packed recurrence at register width LB.
+int emul_pair_scores(int flavor, int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0,
+                     const uint8_t *b1, int lb1, int match, int mismatch, int gap,
+                     int *s0, int *s1)
+{
+    if (LB < 1 || LB > 32 || lb0 > LB || lb1 > LB || la < 1 || lb0 < 1 || lb1 < 1) return -1;
+    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap);
+    uint32_t v = flavor == 0 ? dispatch<0>(LB, a, la, b0, lb0, b1, lb1, sc)
+                             : dispatch<1>(LB, a, la, b0, lb0, b1, lb1, sc);
+    *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
+    *s1 = nwap_unbias(v >> 16, la, lb1, sc);
+    return 0;
+}
+
+int64_t emul_row_of(int64_t idx, int64_t n) { return nwap_row_of(idx, n); }
+int64_t emul_col_of(int64_t idx, int64_t n, int64_t r) { return nwap_col_of(idx, n, r); }
+
+int64_t emul_units_before_group(int64_t n, int gb, int64_t g)
+{
+    nwap_unit_space u; u.n = n; u.S = (n + NWAP_C - 1) / NWAP_C; u.gb = gb; u.gpk = (NWAP_C / NWAP_R) / gb;
+    return nwap_units_before_group(u, g);
+}
+
+void emul_unit_decode(int64_t n, int gb, int64_t t, int64_t *group, int64_t *strip)
+{
+    nwap_unit_space u; u.n = n; u.S = (n + NWAP_C - 1) / NWAP_C; u.gb = gb; u.gpk = (NWAP_C / NWAP_R) / gb;
+    nwap_unit_decode(u, t, group, strip);
+}
+
+int emul_geometry(int *R, int *C, int *chunk) { *R = NWAP_R; *C = NWAP_C; *chunk = NWAP_CHUNK; return 0; }
+}

@@ -1,0 +1,171 @@
+"""Pins the CPU oracle (oracle/) against vectors produced by the unmodified Python
+reference (tests/golden/make_golden.py) and the known answers in the reference's
+own tests.  CPU only."""
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import nw_oracle as orc
+from paper_2509_01654_b200 import synth
+from conftest import GOLDEN
+
+
+def _sim(case, size=None):
+    m, x, g = case["scheme"]
+    ov = {(a, b): v for a, b, v in case.get("overrides", [])}
+    size = int(case["ids"].max()) + 1 if size is None else size
+    return orc.similarity_matrix(m, x, size, ov), g
+
+
+# ---- known answers held by the reference tests -------------------------------------------
+
+def test_kat_paper_values(golden_kat):
+    # tests/test_aligner.py:41-52, tests/test_engine.py:64-71
+    assert golden_kat["puissance_nuance_1_-1_-2"] == -2
+    assert golden_kat["puisant_paysans_1_-1_-1"] == 3
+    assert golden_kat["puisant_epuisant_1_-1_-1"] == 4
+    assert golden_kat["test_engine_pair"] == -2
+    sim = orc.similarity_matrix(1, -1, 64)
+    assert orc.c_nw_score([0, 18, 16, 11, 26, 11], [29, 18, 26, 11], sim, -2) == -2
+    f = golden_kat["french"]
+    assert orc.c_nw_score(f["puissance"], f["nuance"], sim, -2) == -2
+    assert orc.c_nw_score(f["puisant"], f["paysans"], sim, -1) == 3
+    assert orc.c_nw_score(f["puisant"], f["épuisant"], sim, -1) == 4
+
+
+def test_scalar_cases_match_reference(golden_kat):
+    for c in golden_kat["scalar_cases"]:
+        m, x, g = c["scheme"]
+        sim = orc.similarity_matrix(m, x, 8)
+        assert orc.c_nw_score(c["a"], c["b"], sim, g) == c["score"], c
+
+
+def test_identical_words_and_two_word_payload():
+    # tests/test_engine.py:64-81
+    ids = np.tile(np.array([3, 1, 4, 1, 5], dtype=np.int32), (6, 1))
+    lens = np.full(6, 5, dtype=np.int32)
+    payload, s, mn, mx = orc.c_score_range(ids, lens, orc.similarity_matrix(1, -1, 6), -1, 6, 0, 15)
+    assert payload.tobytes() == bytes([5]) * 15 and mn == mx == 5 and s == 75
+    ids, lens = orc.pack_words([(0, 18, 16, 11, 26, 11), (29, 18, 26, 11)])
+    payload, *_ = orc.c_score_range(ids, lens, orc.similarity_matrix(1, -1, 30), -2, 2, 0, 1)
+    assert payload.tobytes() == b"\xfe"
+
+
+def test_override_case():
+    # tests/test_engine.py:116-125
+    ids, lens = orc.pack_words([(0, 1), (0, 2)])
+    sim = orc.similarity_matrix(1, -1, 3, {(1, 2): 1})
+    payload, *_ = orc.c_score_range(ids, lens, sim, -1, 2, 0, 1)
+    assert payload.tobytes() == bytes([2])
+
+
+# ---- engine payloads from the reference ---------------------------------------------------
+
+def test_engine_cases_c_oracle(golden_cases):
+    for name, c in golden_cases.items():
+        sim, g = _sim(c)
+        n = len(c["lengths"])
+        ids = c["ids"].astype(np.int32)
+        lens = c["lengths"].astype(np.int32)
+        payload, s, mn, mx = orc.c_score_range(ids, lens, sim, g, n, 0, orc.num_edges(n))
+        assert np.array_equal(payload, c["payload"]), name
+        assert (mn, mx) == (c["min"], c["max"]), name
+        assert s / c["edges"] == c["mean"], name
+        assert hashlib.blake2b(payload.tobytes(), digest_size=8).hexdigest() == c["digest"]
+        # threads / chunking never change a byte (tests/test_engine.py:92-101)
+        p2, s2, mn2, mx2 = orc.c_score_range(ids, lens, sim, g, n, 0, orc.num_edges(n), threads=3, chunk=7)
+        assert np.array_equal(p2, payload) and (s2, mn2, mx2) == (s, mn, mx)
+
+
+def test_engine_cases_numpy_port(golden_cases):
+    for name in ("seed9", "seed4", "gap0", "gappos", "mis_gt_match", "override", "long40"):
+        c = golden_cases[name]
+        sim, g = _sim(c)
+        n = len(c["lengths"])
+        payload, s, mn, mx = orc.np_score_range(c["ids"].astype(np.int32), c["lengths"].astype(np.int32),
+                                                sim, g, n, 0, orc.num_edges(n))
+        assert np.array_equal(payload, c["payload"]), name
+        assert (mn, mx) == (c["min"], c["max"])
+
+
+def test_numpy_port_pool_matches(golden_cases):
+    c = golden_cases["seed500"]
+    sim, g = _sim(c)
+    n = 500
+    P = orc.num_edges(n)
+    ranges = [(s, min(s + 8192, P)) for s in range(0, P, 8192)]
+    res = orc.np_score_ranges_pool(c["ids"].astype(np.int32), c["lengths"].astype(np.int32), sim, g, n, ranges, 2)
+    payload = np.frombuffer(b"".join(r[0] for r in res), dtype=np.int8)
+    assert np.array_equal(payload, c["payload"])
+
+
+def test_c1_full_config(golden_samples):
+    meta, _ = golden_samples
+    ref = np.load(GOLDEN / "c1.npz")["payload"]
+    ids, lens, sch = synth.config_store("C1")
+    assert synth.store_digest(ids, lens) == meta["C1"]["store_digest"]
+    sim = orc.similarity_matrix(sch[0], sch[1], int(ids.max()) + 1)
+    payload, s, mn, mx = orc.c_all_pairs(ids.astype(np.int32), lens.astype(np.int32), sim, sch[2], threads=4)
+    assert np.array_equal(payload, ref)
+    assert (s, mn, mx) == (meta["C1"]["sum"], meta["C1"]["min"], meta["C1"]["max"])
+    assert hashlib.blake2b(payload.tobytes(), digest_size=8).hexdigest() == meta["C1"]["digest"]
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_sampled_ranges_big_configs(golden_samples, cfg):
+    meta, arrays = golden_samples
+    m = meta[cfg]
+    ids, lens, sch = synth.config_store(cfg)
+    assert synth.store_digest(ids, lens) == m["store_digest"], "synthetic generator drifted"
+    assert synth.total_cells(lens) == m["total_cells"] == orc.total_cells(lens)
+    sim = orc.similarity_matrix(sch[0], sch[1], int(ids.max()) + 1)
+    ids32, len32 = ids.astype(np.int32), lens.astype(np.int32)
+    for k, r in enumerate(m["ranges"]):
+        payload, s, mn, mx = orc.c_score_range(ids32, len32, sim, sch[2], m["n"], r["start"], r["end"])
+        assert np.array_equal(payload, arrays[f"{cfg}_{k}"]), (cfg, k)
+        assert (s, mn, mx) == (r["sum"], r["min"], r["max"])
+
+
+# ---- triangle ------------------------------------------------------------------------------
+
+def test_triangle_against_reference(golden_triangle):
+    t = golden_triangle
+    for n in (4, 300, 10 ** 5, 10 ** 6, 10 ** 7, 600_000):
+        idx, rows, cols = t[f"n{n}_idx"], t[f"n{n}_rows"], t[f"n{n}_cols"]
+        r1, c1 = orc.c_rows_cols(idx, n)
+        assert np.array_equal(r1, rows) and np.array_equal(c1, cols)
+        r2 = orc.np_rows_of(idx, n)
+        assert np.array_equal(r2, rows) and np.array_equal(orc.np_cols_of(idx, n, r2), cols)
+    # tests/test_triangle.py:56-71 literals
+    assert list(t["n4_rows"]) == [0, 0, 0, 1, 1, 2]
+    assert orc.c_rows_cols(np.array([4_999_949_999]), 100_000) == (np.array([99998]), np.array([99999]))
+    assert orc.num_edges(600_000) == 179_999_700_000 and orc.num_edges(100_000) == 4_999_950_000
+
+
+def test_preflight_bounds():
+    # tests/test_engine.py:41-54
+    q, lo, hi = orc.preflight(np.array([70, 2]), -2, -1, 1)
+    assert q == 0 and lo == -280
+    q, lo, hi = orc.preflight(np.array([20]), -1, -1, 10)
+    assert q == 0 and hi == 200
+    assert orc.preflight(np.array([3, 9, 4]), -1, -1, 1)[0] == 9
+
+
+def test_cells_and_equal_work_bounds():
+    rng = np.random.default_rng(5)
+    lens = rng.integers(1, 12, size=57).astype(np.int32)
+    n = 57
+    P = orc.num_edges(n)
+    assert orc.cells_in_range(lens, n, 0, P) == orc.total_cells(lens)
+    # brute-force definition of the bounds
+    r, c = orc.c_rows_cols(np.arange(P), n)
+    work = np.concatenate([[0], np.cumsum(lens[r].astype(np.int64) * lens[c])])
+    for parts in (1, 2, 3, 8):
+        b = orc.np_equal_work_bounds(lens, parts)
+        W = int(work[-1])
+        for g in range(1, parts):
+            target = -((-g * W) // parts)
+            assert b[g] == int(np.searchsorted(work, target, side="left"))
+        assert b[0] == 0 and b[-1] == P
