@@ -1,0 +1,117 @@
+"""CPU checks of the device headers compiled as plain C++ (tests/native/host_emul.cpp):
+the packed s16x2 recurrence (csrc/nwap_core.cuh) against the oracle, the device index
+recovery (csrc/nwap_index.cuh) against the reference vectors, and the work-unit
+enumeration of the tile kernel."""
+import ctypes
+import random
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import nw_oracle as orc
+
+ROOT = Path(__file__).resolve().parent.parent
+SRC = ROOT / "tests" / "native" / "host_emul.cpp"
+SO = ROOT / "tests" / "native" / "libhost_emul.so"
+
+
+@pytest.fixture(scope="module")
+def emul():
+    hdrs = list((ROOT / "paper_2509_01654_b200" / "csrc").glob("*.cuh"))
+    newest = max(p.stat().st_mtime for p in [SRC, *hdrs])
+    if not SO.exists() or SO.stat().st_mtime < newest:
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wno-unknown-pragmas",
+                               "-I", str(ROOT / "paper_2509_01654_b200" / "csrc"), "-o", str(SO), str(SRC)])
+    L = ctypes.CDLL(str(SO))
+    p, i, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    L.emul_pair_scores.argtypes = [i, i, p, i, p, i, p, i, i, i, i, p, p]
+    L.emul_row_of.restype = i64
+    L.emul_row_of.argtypes = [i64, i64]
+    L.emul_col_of.restype = i64
+    L.emul_col_of.argtypes = [i64, i64, i64]
+    L.emul_units_before_group.restype = i64
+    L.emul_units_before_group.argtypes = [i64, i, i64]
+    L.emul_unit_decode.argtypes = [i64, i, i64, p, p]
+    L.emul_geometry.argtypes = [p, p, p]
+    return L
+
+
+def _random_scheme(rng, q):
+    while True:
+        m, x, g = rng.randint(-3, 4), rng.randint(-4, 4), rng.randint(-4, 3)
+        lo = min(0, 2 * q * g, q * min(m, x))
+        hi = max(0, 2 * q * g, q * max(m, x))
+        if lo >= -128 and hi <= 127:
+            return m, x, g
+
+
+@pytest.mark.parametrize("flavor", [0, 1])
+def test_packed_recurrence_matches_oracle(emul, flavor):
+    rng = random.Random(1234 + flavor)
+    for _ in range(6000):
+        q = rng.randint(1, 32)
+        m, x, g = _random_scheme(rng, q)
+        K = rng.choice([2, 3, 5, 40, 255])
+        la, lb0, lb1 = rng.randint(1, q), rng.randint(1, q), rng.randint(1, q)
+        LB = rng.randint(max(lb0, lb1), q)
+        a = np.array([rng.randrange(K) for _ in range(la)], dtype=np.uint8)
+        b0 = np.array([rng.randrange(K) for _ in range(lb0)], dtype=np.uint8)
+        b1 = np.array([rng.randrange(K) for _ in range(lb1)], dtype=np.uint8)
+        sim = orc.similarity_matrix(m, x, 256)
+        s0, s1 = ctypes.c_int(), ctypes.c_int()
+        assert emul.emul_pair_scores(flavor, LB, a.ctypes.data, la, b0.ctypes.data, lb0, b1.ctypes.data, lb1,
+                                     m, x, g, ctypes.addressof(s0), ctypes.addressof(s1)) == 0
+        assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim, g), orc.c_nw_score(a, b1, sim, g)), \
+            (LB, m, x, g, a, b0, b1)
+
+
+def test_packed_recurrence_extreme_schemes(emul):
+    # the largest magnitudes the int8 preflight admits at each length
+    rng = random.Random(7)
+    for q, (m, x, g) in [(32, (3, -4, -2)), (32, (-4, 3, -2)), (21, (6, -6, -3)), (16, (7, -8, -4)),
+                         (32, (3, 3, 1)), (8, (15, -16, -8)), (1, (127, -128, -64)), (32, (0, 0, 0)),
+                         (4, (31, -32, 15))]:
+        sim = orc.similarity_matrix(m, x, 4)
+        for _ in range(300):
+            la, lb0, lb1 = rng.randint(1, q), rng.randint(1, q), rng.randint(1, q)
+            a = np.array([rng.randrange(3) for _ in range(la)], dtype=np.uint8)
+            b0 = np.array([rng.randrange(3) for _ in range(lb0)], dtype=np.uint8)
+            b1 = np.array([rng.randrange(3) for _ in range(lb1)], dtype=np.uint8)
+            for fl in (0, 1):
+                s0, s1 = ctypes.c_int(), ctypes.c_int()
+                emul.emul_pair_scores(fl, max(lb0, lb1), a.ctypes.data, la, b0.ctypes.data, lb0,
+                                      b1.ctypes.data, lb1, m, x, g, ctypes.addressof(s0), ctypes.addressof(s1))
+                assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim, g), orc.c_nw_score(a, b1, sim, g))
+
+
+def test_device_index_recovery_matches_reference(emul, golden_triangle):
+    t = golden_triangle
+    for n in (4, 300, 10 ** 5, 10 ** 6, 10 ** 7, 600_000):
+        idx, rows, cols = t[f"n{n}_idx"], t[f"n{n}_rows"], t[f"n{n}_cols"]
+        for k in range(0, len(idx), max(1, len(idx) // 700)):
+            r = emul.emul_row_of(int(idx[k]), n)
+            assert r == rows[k] and emul.emul_col_of(int(idx[k]), n, r) == cols[k]
+
+
+@pytest.mark.parametrize("n,gb", [(5000, 1), (5000, 4), (20_000, 2), (70_001, 16), (600_000, 16), (2049, 1), (2048, 8)])
+def test_unit_enumeration_is_a_bijection(emul, n, gb):
+    R, C, CH = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    emul.emul_geometry(ctypes.addressof(R), ctypes.addressof(C), ctypes.addressof(CH))
+    R, C = R.value, C.value
+    S = -(-n // C)
+    groups = -(-(n - 1) // (gb * R))
+    total = emul.emul_units_before_group(n, gb, groups)
+    # expected: group g owns strips (g*gb*R)//C .. S-1
+    expect = sum(S - (g * gb * R) // C for g in range(groups))
+    assert total == expect
+    step = max(1, total // 4000)
+    g_, s_ = ctypes.c_int64(), ctypes.c_int64()
+    probe = list(range(0, total, step)) + [total - 1]
+    for t in probe:
+        emul.emul_unit_decode(n, gb, t, ctypes.addressof(g_), ctypes.addressof(s_))
+        g, s = g_.value, s_.value
+        k = (g * gb * R) // C
+        assert 0 <= g < groups and k <= s < S
+        assert emul.emul_units_before_group(n, gb, g) + (s - k) == t

@@ -1,0 +1,363 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle, the reference's golden
+vectors and the reference tests' own cases.  Bit-exact: this is integer/byte work."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2509_01654_b200 as nw
+from paper_2509_01654_b200 import _native, synth
+from paper_2509_01654_b200.engine import NwapContext, device_rows_cols
+from oracle import nw_oracle as orc
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+FAST = ["packed", "packed3"]
+ALL = ["packed", "packed3", "simple"]
+
+
+class CollectSink:
+    def __init__(self, fail_at=None):
+        self.chunks, self.aborted, self.fail_at = [], False, fail_at
+
+    def write(self, data):
+        if self.fail_at is not None and len(self.chunks) >= self.fail_at:
+            raise OSError("disk full")
+        self.chunks.append(bytes(data))
+
+    def abort(self):
+        self.aborted = True
+
+    @property
+    def payload(self):
+        return b"".join(self.chunks)
+
+
+def _scheme(case):
+    m, x, g = case["scheme"]
+    return nw.ScoringScheme(m, x, g, overrides={(a, b): v for a, b, v in case.get("overrides", [])})
+
+
+def _score(ctx, start, end, variant, offset=0, want_hist=False):
+    buf = torch.full((end - start + offset + 64,), 0x55, dtype=torch.int8, device="cuda")
+    out = buf[offset:]
+    st = ctx.score_range(start, end, out, want_hist=want_hist, variant=variant)
+    torch.cuda.synchronize()
+    host = buf.cpu().numpy()
+    # nothing outside [offset, offset + end - start) may be touched
+    assert (host[:offset] == 0x55).all() and (host[offset + end - start:] == 0x55).all()
+    return host[offset: offset + end - start], st
+
+
+def _oracle(ids, lens, scheme, start, end, threads=1):
+    m, x, g = scheme.match, scheme.mismatch, scheme.gap
+    sim = orc.similarity_matrix(m, x, int(ids.max()) + 1, dict(scheme.overrides))
+    return orc.c_score_range(ids.astype(np.int32), lens.astype(np.int32), sim, g, len(lens), start, end,
+                             threads=threads)
+
+
+def test_library_is_the_cuda_one():
+    assert _native.lib().nwap_device_count() >= 1
+    assert torch.cuda.get_device_capability(0)[0] >= 10
+
+
+# ---- the reference tests' own cases (tests/test_engine.py) --------------------------------
+
+def test_two_word_payload_is_single_byte():
+    words = [nw.EncodedWord("puissance", "x", (0, 18, 16, 11, 26, 11), 1.0),
+             nw.EncodedWord("nuance", "y", (29, 18, 26, 11), 1.0)]
+    sink = CollectSink()
+    nw.compute_all_pairs(words, nw.ScoringScheme(1, -1, -2), sink)
+    assert sink.payload == b"\xfe"
+
+
+def test_identical_words_score_their_length():
+    words = [nw.EncodedWord(f"w{i}", f"i{i}", (3, 1, 4, 1, 5), 1.0) for i in range(6)]
+    sink = CollectSink()
+    stats = nw.compute_all_pairs(words, nw.ScoringScheme(), sink)
+    assert sink.payload == bytes([5]) * 15
+    assert stats.min_score == stats.max_score == 5 and stats.mean_score == 5.0 and stats.edges_written == 15
+
+
+def test_scheme_overrides_respected():
+    words = [nw.EncodedWord("a", "a", (0, 1), 1.0), nw.EncodedWord("b", "b", (0, 2), 1.0)]
+    sink = CollectSink()
+    nw.compute_all_pairs(words, nw.ScoringScheme(1, -1, -1, overrides={(1, 2): 1}), sink)
+    assert sink.payload == bytes([2])
+
+
+@pytest.mark.parametrize("chunk_size", [7, 64, 1024, 10 ** 6])
+def test_payload_independent_of_partitioning(golden_cases, chunk_size):
+    c = golden_cases["seed4"]
+    words = synth.make_words(40, seed=4, alphabet=10)
+    scheme = nw.ScoringScheme(2, -1, -2)
+    sink = CollectSink()
+    plan = nw.ComputePlan(n=40, chunk_size=chunk_size, worker_count=2, scheme=scheme)
+    nw.compute_all_pairs(words, scheme, sink, plan)
+    assert sink.payload == c["payload"].tobytes()
+    assert all(len(ch) <= chunk_size for ch in sink.chunks)
+
+
+def test_stats_are_exact(golden_cases):
+    c = golden_cases["seed11"]
+    sink = CollectSink()
+    stats = nw.compute_all_pairs(synth.make_words(25, seed=11), nw.ScoringScheme(), sink)
+    scores = np.frombuffer(sink.payload, dtype=np.int8)
+    assert np.array_equal(scores, c["payload"])
+    assert stats.edges_written == 300 and stats.min_score == c["min"] and stats.max_score == c["max"]
+    assert stats.mean_score == c["mean"] == float(scores.astype(np.int64).mean())
+
+
+def test_sink_failure_aborts():
+    sink = CollectSink(fail_at=1)
+    with pytest.raises(OSError):
+        nw.compute_all_pairs(synth.make_words(40, seed=4), nw.ScoringScheme(), sink, nw.ComputePlan(n=40, chunk_size=100))
+    assert sink.aborted
+
+
+def test_errors_surface_as_reference_exceptions():
+    with pytest.raises(nw.DataError, match="-280"):
+        nw.compute_all_pairs([nw.EncodedWord("l", "x", tuple([0] * 70), 1.0), nw.EncodedWord("s", "y", (0, 1), 1.0)],
+                             nw.ScoringScheme(1, -1, -2), CollectSink())
+    ids = np.zeros((3, 4), dtype=np.uint8)
+    with pytest.raises(ValueError, match="empty"):
+        NwapContext(ids, np.array([2, 0, 1], dtype=np.uint8), nw.ScoringScheme())
+    with pytest.raises(nw.DataError):
+        NwapContext(np.zeros((2, 70), dtype=np.uint8), np.array([70, 2], dtype=np.uint8), nw.ScoringScheme(1, -1, -2))
+    with NwapContext(np.zeros((4, 40), dtype=np.uint8), np.full(4, 40, dtype=np.uint8), nw.ScoringScheme()) as ctx:
+        out = torch.empty(6, dtype=torch.int8, device="cuda")
+        with pytest.raises(ValueError, match="packed kernel"):
+            ctx.score_range(0, 6, out, variant="packed")
+        with pytest.raises(ValueError):
+            ctx.score_range(0, 7, torch.empty(7, dtype=torch.int8, device="cuda"))
+
+
+# ---- golden engine payloads, every kernel variant ------------------------------------------
+
+@pytest.mark.parametrize("name", ["seed9", "seed4", "seed11", "seed30", "seed500", "gap0", "gappos",
+                                  "mis_gt_match", "long40", "override"])
+def test_golden_engine_cases(golden_cases, name):
+    c = golden_cases[name]
+    scheme = _scheme(c)
+    n = len(c["lengths"])
+    P = nw.num_edges(n)
+    with NwapContext(c["ids"], c["lengths"], scheme) as ctx:
+        variants = ["simple"] if (c.get("overrides") or ctx.max_len > 32) else ALL
+        for v in variants + ["auto"]:
+            got, st = _score(ctx, 0, P, v, want_hist=True)
+            assert np.array_equal(got, c["payload"]), (name, v)
+            ssum, smin, smax, scount, hist = st
+            assert (smin, smax, scount) == (c["min"], c["max"], P)
+            assert ssum / P == c["mean"]
+            assert np.array_equal(hist, orc.np_histogram(c["payload"]))
+            assert hashlib.blake2b(got.tobytes(), digest_size=8).hexdigest() == c["digest"]
+
+
+@pytest.mark.parametrize("variant", ALL)
+def test_arbitrary_subranges_and_alignments(golden_cases, variant):
+    c = golden_cases["seed500"]
+    n, P = 500, nw.num_edges(500)
+    rng = np.random.default_rng(3)
+    with NwapContext(c["ids"], c["lengths"], _scheme(c)) as ctx:
+        cases = [(0, 1), (P - 1, P), (0, 499), (498, 500), (499, 499 + 498), (P - 3, P), (7, 7)]
+        for _ in range(40):
+            s = int(rng.integers(0, P))
+            e = int(min(P, s + rng.integers(1, 30_000)))
+            cases.append((s, e))
+        for k, (s, e) in enumerate(cases):
+            got, st = _score(ctx, s, e, variant, offset=k % 17)
+            assert np.array_equal(got, c["payload"][s:e]), (s, e)
+            if e > s:
+                ref = c["payload"][s:e].astype(np.int64)
+                assert st[:4] == (int(ref.sum()), int(ref.min()), int(ref.max()), e - s)
+            else:
+                assert st[:4] == (0, 127, -128, 0)
+
+
+@pytest.mark.parametrize("variant", FAST)
+def test_length_extremes(variant):
+    rng = np.random.default_rng(11)
+    for n, lo, hi, sch in [(2, 1, 1, (1, -1, -1)), (3, 32, 32, (1, -1, -2)), (700, 1, 32, (1, -1, -2)),
+                           (2100, 1, 3, (2, -1, -3)), (2060, 30, 32, (1, -1, -1)), (4100, 1, 16, (3, -2, -4))]:
+        lens = rng.integers(lo, hi + 1, size=n).astype(np.uint8)
+        ids = rng.integers(0, 5, size=(n, hi)).astype(np.uint8)
+        scheme = nw.ScoringScheme(*sch)
+        P = nw.num_edges(n)
+        ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P, threads=4)
+        with NwapContext(ids, lens, scheme) as ctx:
+            got, st = _score(ctx, 0, P, variant)
+            assert np.array_equal(got, ref), (n, lo, hi)
+            assert st[:4] == (rsum, rmin, rmax, P)
+
+
+def test_random_schemes_all_variants():
+    rng = np.random.default_rng(2024)
+    for trial in range(12):
+        q = int(rng.integers(2, 33))
+        while True:
+            m, x, g = int(rng.integers(-3, 5)), int(rng.integers(-4, 5)), int(rng.integers(-4, 4))
+            if min(0, 2 * q * g, q * min(m, x)) >= -128 and max(0, 2 * q * g, q * max(m, x)) <= 127:
+                break
+        n = int(rng.integers(40, 400))
+        lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
+        lens[0] = q
+        ids = rng.integers(0, int(rng.integers(2, 41)), size=(n, q)).astype(np.uint8)
+        scheme = nw.ScoringScheme(m, x, g)
+        P = nw.num_edges(n)
+        ref, *_ = _oracle(ids, lens, scheme, 0, P)
+        with NwapContext(ids, lens, scheme) as ctx:
+            for v in ALL:
+                got, _ = _score(ctx, 0, P, v)
+                assert np.array_equal(got, ref), (trial, v, (m, x, g), q)
+
+
+# ---- BASELINE.json configs -------------------------------------------------------------------
+
+def test_c1_full_config_through_entry_point(golden_samples):
+    meta, _ = golden_samples
+    ref = np.load(GOLDEN / "c1.npz")["payload"]
+    ids, lens, sch = synth.config_store("C1")
+    words = synth.as_encoded_words(ids, lens)
+    sink = CollectSink()
+    stats = nw.compute_all_pairs(words, nw.ScoringScheme(*sch), sink)
+    assert sink.payload == ref.tobytes()
+    assert (stats.min_score, stats.max_score, stats.mean_score) == (meta["C1"]["min"], meta["C1"]["max"], meta["C1"]["mean"])
+    assert hashlib.blake2b(sink.payload, digest_size=8).hexdigest() == meta["C1"]["digest"]
+
+
+def test_c2_every_byte_against_oracle(golden_samples):
+    """configs[1]: 20,000 words, all 199,990,000 pairs bit-exact vs the CPU oracle."""
+    ids, lens, sch = synth.config_store("C2")
+    scheme = nw.ScoringScheme(*sch)
+    n = len(lens)
+    P = nw.num_edges(n)
+    ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P, threads=0 or len(__import__("os").sched_getaffinity(0)))
+    with NwapContext(ids, lens, scheme) as ctx:
+        for v in ALL:
+            out = torch.empty(P, dtype=torch.int8, device="cuda")
+            st = ctx.score_range(0, P, out, want_hist=True, variant=v)
+            got = out.cpu().numpy()
+            assert np.array_equal(got, ref), v
+            assert st[:4] == (rsum, rmin, rmax, P)
+            assert np.array_equal(st[4], orc.np_histogram(ref))
+        # host-destination pipeline (the e2e call) and the independent statistics kernel
+        host = torch.empty(P, dtype=torch.int8).pin_memory()
+        st = ctx.score_range_host(0, P, host, want_hist=True)
+        assert np.array_equal(host.numpy(), ref) and st[:4] == (rsum, rmin, rmax, P)
+        ps = ctx.payload_stats(out)
+        assert ps[:4] == (rsum, rmin, rmax, P) and np.array_equal(ps[4], orc.np_histogram(ref))
+        # equal-work shards written independently reproduce the payload (multi-GPU path, one GPU)
+        bounds = ctx.equal_work_bounds(8)
+        from paper_2509_01654_b200 import sharding
+        assert np.array_equal(bounds, sharding.equal_work_bounds(lens, 8))
+        whole = torch.zeros(P, dtype=torch.int8, device="cuda")
+        tot = 0
+        for g in range(8):
+            s, e = int(bounds[g]), int(bounds[g + 1])
+            stg = ctx.score_range(s, e, whole[s:e])
+            tot += stg[0]
+        assert np.array_equal(whole.cpu().numpy(), ref) and tot == rsum
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_sampled_ranges_of_big_configs(golden_samples, cfg):
+    """configs[2..4]: ranges scored by the reference's _score_range (golden) byte for byte."""
+    meta, arrays = golden_samples
+    m = meta[cfg]
+    ids, lens, sch = synth.config_store(cfg)
+    assert synth.store_digest(ids, lens) == m["store_digest"]
+    with NwapContext(ids, lens, nw.ScoringScheme(*sch)) as ctx:
+        for k, r in enumerate(m["ranges"]):
+            for v in ALL:
+                got, st = _score(ctx, r["start"], r["end"], v, offset=k)
+                assert np.array_equal(got, arrays[f"{cfg}_{k}"]), (cfg, k, v)
+                assert st[:3] == (r["sum"], r["min"], r["max"])
+        # equal-work bounds agree between the library and the host mirror
+        from paper_2509_01654_b200 import sharding
+        assert np.array_equal(ctx.equal_work_bounds(8), sharding.equal_work_bounds(lens, 8))
+        assert ctx.cells_in_range(0, ctx.num_edges) == m["total_cells"]
+
+
+def test_c3_two_independent_kernels_agree():
+    """configs[2] at full size (4,999,950,000 pairs): the packed DPX kernel and the int32
+    one-thread-per-pair kernel must produce the same histogram / sum / min / max, and the same
+    bytes on a strided sample of slabs."""
+    ids, lens, sch = synth.config_store("C3")
+    with NwapContext(ids, lens, nw.ScoringScheme(*sch)) as ctx:
+        P = ctx.num_edges
+        a = torch.empty(P, dtype=torch.int8, device="cuda")
+        sa = ctx.score_range(0, P, a, want_hist=True, variant="packed")
+        assert sa[3] == P
+        ps = ctx.payload_stats(a)
+        assert ps[:4] == sa[:4] and np.array_equal(ps[4], sa[4])
+        slab = 250_000_000
+        b = torch.empty(slab, dtype=torch.int8, device="cuda")
+        tot = [0, 127, -128, 0]
+        hist = np.zeros(256, dtype=np.int64)
+        for s in range(0, P, slab):
+            e = min(P, s + slab)
+            sb = ctx.score_range(s, e, b, want_hist=True, variant="simple")
+            assert torch.equal(a[s:e], b[: e - s]), s
+            tot = [tot[0] + sb[0], min(tot[1], sb[1]), max(tot[2], sb[2]), tot[3] + sb[3]]
+            hist += sb[4]
+        assert tuple(tot) == sa[:4] and np.array_equal(hist, sa[4])
+
+
+# ---- new surface: compaction, degree, index recovery ----------------------------------------
+
+def test_compaction_and_degree(golden_cases):
+    c = golden_cases["seed500"]
+    n, P = 500, nw.num_edges(500)
+    with NwapContext(c["ids"], c["lengths"], _scheme(c)) as ctx:
+        out = torch.empty(P, dtype=torch.int8, device="cuda")
+        ctx.score_range(0, P, out)
+        for thr, (s, e) in [(2, (0, P)), (0, (1234, 99_000)), (-3, (P - 5000, P)), (100, (0, P))]:
+            degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+            idx, sc = ctx.compact_range(out[s:e], s, e, thr, capacity=e - s, degree=degree)
+            ridx, rsc, rdeg = orc.np_compact(c["payload"][s:e], s, n, thr)
+            assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
+            assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
+        with pytest.raises(_native.CapacityError) as ei:
+            ctx.compact_range(out, 0, P, 0, capacity=10)
+        assert ei.value.count == int((c["payload"] >= 0).sum())
+
+
+def test_c5_threshold_compaction_slab(golden_samples):
+    """configs[4]: alternate scheme (2,-1,-3), keep score >= 4, on a slab of the 600k job."""
+    ids, lens, sch = synth.config_store("C5")
+    n = len(lens)
+    with NwapContext(ids, lens, nw.ScoringScheme(*sch)) as ctx:
+        P = ctx.num_edges
+        s, e = P // 3, P // 3 + 3_000_000
+        out = torch.empty(e - s, dtype=torch.int8, device="cuda")
+        ctx.score_range(s, e, out)
+        ref, *_ = _oracle(ids, lens, nw.ScoringScheme(*sch), s, e, threads=8)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+        idx, sc = ctx.compact_range(out, s, e, synth.C5_THRESHOLD, capacity=e - s, degree=degree)
+        ridx, rsc, rdeg = orc.np_compact(ref, s, n, synth.C5_THRESHOLD)
+        assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
+        assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
+
+
+def test_device_index_recovery(golden_triangle):
+    t = golden_triangle
+    for n in (4, 300, 10 ** 5, 10 ** 6, 10 ** 7, 600_000):
+        rows, cols = device_rows_cols(t[f"n{n}_idx"], n)
+        assert np.array_equal(rows, t[f"n{n}_rows"]) and np.array_equal(cols, t[f"n{n}_cols"])
+    # exhaustive bijection for small n (tests/test_acceptance.py:136-153)
+    for n in (2, 3, 17, 129, 300):
+        idx = np.arange(nw.num_edges(n), dtype=np.int64)
+        rows, cols = device_rows_cols(idx, n)
+        assert (rows < cols).all() and (cols <= n - 1).all()
+        assert np.array_equal(rows * (2 * n - rows - 1) // 2 + (cols - rows - 1), idx)
+
+
+def test_launch_counter_moves():
+    before = _native.lib().nwap_launch_count()
+    c_ids = np.ones((10, 3), dtype=np.uint8)
+    with NwapContext(c_ids, np.full(10, 3, dtype=np.uint8), nw.ScoringScheme()) as ctx:
+        ctx.score_range(0, 45, torch.empty(45, dtype=torch.int8, device="cuda"))
+    assert _native.lib().nwap_launch_count() >= before + 2
