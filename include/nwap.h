@@ -149,9 +149,13 @@ int nwap_rows_cols(int64_t n, const int64_t *idx_dev, int64_t count,
 #define NWAP_PROBE_IMAD            3
 #define NWAP_PROBE_LOP3            4
 #define NWAP_PROBE_IADD3           5
-#define NWAP_PROBE_MIX_2ALU_2IMAD  6   /* the packed cell's instruction mix */
+#define NWAP_PROBE_MIX_2ALU_2IMAD  6   /* the packed cell's instruction mix: 2 DPX + 2 IMAD */
 #define NWAP_PROBE_MIX_3ALU_1IMAD  7
-#define NWAP_PROBE_COUNT           8
+/* 8..21: single-op and two-pipe mixes used to establish the port model
+ * (add.u16x2, min.u16x2, fma.f16x2, max.f16x2, prmt, DPX+IADD, DPX+VIMNMX2, IMAD+IADD,
+ *  IMAD+HFMA2, DPX+IMAD, alternative cell formulations, VIADDMNMX+VIMNMX3) -- names in
+ * paper_2509_01654_b200/_native.py:PROBES. */
+#define NWAP_PROBE_COUNT           22
 int nwap_probe(int device, int which, int iters, double *ipc_out, double *ms_out);
 
 /* Kernels launched by this library on the calling process so far. */

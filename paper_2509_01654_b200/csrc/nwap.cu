@@ -70,17 +70,18 @@ struct nwap_ctx {
     int64_t slab_bytes = 0;
     cudaStream_t s_compute = nullptr, s_copy = nullptr;
     cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
-    int occ_tiles[4] = {0, 0, 0, 0};    // resident CTAs/SM per (flavor, qw) instantiation
+    int occ_tiles[6] = {0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor, qclass) instantiation
 };
 
 namespace {
 
 typedef void (*tile_kernel_t)(const nwap_tile_params);
 
-tile_kernel_t tile_kernel(int flavor, int qw)
+// qclass: 0 -> rows up to 16 symbols, 1 -> up to 24, 2 -> up to 32
+tile_kernel_t tile_kernel(int flavor, int qclass)
 {
-    if (flavor == 0) return qw == 4 ? k_score_tiles<0, 4> : k_score_tiles<0, 8>;
-    return qw == 4 ? k_score_tiles<1, 4> : k_score_tiles<1, 8>;
+    if (flavor == 0) return qclass == 0 ? k_score_tiles<0, 16> : qclass == 1 ? k_score_tiles<0, 24> : k_score_tiles<0, 32>;
+    return qclass == 0 ? k_score_tiles<1, 16> : qclass == 1 ? k_score_tiles<1, 24> : k_score_tiles<1, 32>;
 }
 
 int build_sim_table(nwap_ctx *c, const int8_t *sim_host)
@@ -145,7 +146,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     }
 
     const int flavor = variant == NWAP_VARIANT_PACKED3 ? 1 : 0;
-    const int qw = c->qpad <= 16 ? 4 : 8;
+    const int qclass = c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
     nwap_tile_params p;
     p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad;
     p.start = start; p.end = end;
@@ -158,7 +159,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.stats = c->d_stats; p.want_hist = want_hist;
     p.unit_counter = c->d_counter;
 
-    const int occ = std::max(1, c->occ_tiles[flavor * 2 + (qw == 8 ? 1 : 0)]);
+    const int occ = std::max(1, c->occ_tiles[flavor * 3 + qclass]);
     const int64_t slots = (int64_t)c->sm_count * occ;
     // bands per group: as large as possible (amortises the per-unit sort) while
     // leaving >= 24 units per resident CTA for dynamic balance.
@@ -177,7 +178,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.us = us; p.unit_begin = ubeg; p.unit_count = ucount;
     const int64_t grid = std::min<int64_t>(slots, ucount);
     CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
-    tile_kernel(flavor, qw)<<<(unsigned)grid, NWAP_THREADS, sizeof(nwap_tile_smem), st>>>(p);
+    tile_kernel(flavor, qclass)<<<(unsigned)grid, NWAP_THREADS, sizeof(nwap_tile_smem), st>>>(p);
     g_launches++;
     CK(cudaGetLastError());
     return NWAP_OK;
@@ -268,12 +269,12 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
     }
     if (rc == NWAP_OK) {
         for (int f = 0; f < 2 && rc == NWAP_OK; ++f)
-            for (int w = 0; w < 2 && rc == NWAP_OK; ++w) {
-                tile_kernel_t k = tile_kernel(f, w ? 8 : 4);
+            for (int w = 0; w < 3 && rc == NWAP_OK; ++w) {
+                tile_kernel_t k = tile_kernel(f, w);
                 guard(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(nwap_tile_smem)), "cudaFuncSetAttribute");
                 int occ = 0;
                 guard(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, sizeof(nwap_tile_smem)), "occupancy query");
-                c->occ_tiles[f * 2 + w] = occ;
+                c->occ_tiles[f * 3 + w] = occ;
             }
     }
     if (rc != NWAP_OK) { nwap_destroy(c); return rc; }
@@ -523,8 +524,11 @@ int nwap_probe(int device, int which, int iters, double *ipc_out, double *ms_out
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     typedef void (*probe_t)(int, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t *, long long *);
-    static const probe_t table[NWAP_PROBE_COUNT] = {k_probe<0>, k_probe<1>, k_probe<2>, k_probe<3>,
-                                                    k_probe<4>, k_probe<5>, k_probe<6>, k_probe<7>};
+    static const probe_t table[NWAP_PROBE_COUNT] = {
+        k_probe<0>, k_probe<1>, k_probe<2>, k_probe<3>, k_probe<4>, k_probe<5>, k_probe<6>, k_probe<7>,
+        k_probe<8>, k_probe<9>, k_probe<10>, k_probe<11>, k_probe<12>, k_probe<13>, k_probe<14>, k_probe<15>,
+        k_probe<16>, k_probe<17>, k_probe<18>, k_probe<19>, k_probe<20>, k_probe<21>};
+    static const double per_step[NWAP_PROBE_COUNT] = {1, 1, 1, 1, 1, 1, 4, 4, 1, 1, 1, 1, 1, 2, 2, 2, 2, 2, 4, 5, 5, 2};
     for (int rep = 0; rep < 2; ++rep) {   // first launch warms up
         CK(cudaEventRecord(e0));
         table[which]<<<blocks, 512>>>(iters, 0x00030005u, 0xfffefffdu, 0x00070009u, 1u, sink, cycles);
@@ -539,7 +543,7 @@ int nwap_probe(int device, int which, int iters, double *ipc_out, double *ms_out
     CK(cudaMemcpy(h.data(), cycles, sizeof(long long) * blocks, cudaMemcpyDeviceToHost));
     long long mx = 1;
     for (long long v : h) mx = std::max(mx, v);
-    const double per_thread = which >= 6 ? 4.0 : 1.0;      // instructions per chain step
+    const double per_thread = per_step[which];           // instructions per chain step
     const double warp_instr = (double)iters * 16 * 8 * per_thread * (512 / 32);
     *ipc_out = warp_instr / (double)mx;
     *ms_out = ms;

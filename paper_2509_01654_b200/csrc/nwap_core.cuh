@@ -114,52 +114,61 @@ NWAP_HD uint32_t nwap_pack_negb(uint32_t b0, uint32_t b1)
 }
 
 // One score-matrix row (one symbol of the row word, packed as a*65537) against
-// the LB register-resident columns.  FIRST = this is matrix row 1, whose
-// "previous row" is the constant boundary, so P/PU are written, not read.
-// left0 is H'[i][0] for this row (both halves).
-template <int LB, int FLAVOR, bool FIRST>
-NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t (&nb)[LB], uint32_t (&P)[LB + 1],
-                         uint32_t (&PU)[LB + 1], uint32_t left0, const nwap_scheme_consts &sc)
+// the LB register-resident columns P[1..LB] (P[0] is unused).  d0 = H'[i-1][0],
+// left0 = H'[i][0] (both halves).  The cell is software-pipelined: the diagonal
+// term of cell j+1 is formed from the OLD P[j] before P[j] is overwritten, so the
+// update is in place and the loop over matrix rows needs no register moves and
+// no unrolling -- which keeps the per-length code small enough for the
+// instruction cache (32 length-specialised bodies live in one kernel).
+template <int LB, int FLAVOR>
+NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                         uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc)
 {
-    uint32_t diag = FIRST ? NWAP_BIAS2 : P[0];
-    P[0] = left0;
     uint32_t left = left0;
-    const uint32_t bias_u2 = NWAP_BIAS2 + sc.u2;
+    uint32_t dw = nwap_viaddmin_u16x2(a2, nb[0], 0x00010001u) * sc.neg_delta + d0;
 #pragma unroll
     for (int j = 1; j <= LB; ++j) {
-        uint32_t e = nwap_viaddmin_u16x2(a2, nb[j - 1], 0x00010001u);
-        uint32_t dw = e * sc.neg_delta + diag;
+        uint32_t dw_next = 0;
+        if (j < LB) dw_next = nwap_viaddmin_u16x2(a2, nb[j], 0x00010001u) * sc.neg_delta + P[j];
         uint32_t cur;
         if (FLAVOR == 0) {
-            uint32_t upu = FIRST ? bias_u2 : PU[j];
-            diag = FIRST ? NWAP_BIAS2 : P[j];
+            const uint32_t upu = P[j] * sc.one + sc.u2;
             cur = nwap_vimax3_s16x2(dw, upu, left);
-            PU[j] = cur * sc.one + sc.u2;
         } else {
-            uint32_t up = FIRST ? NWAP_BIAS2 : P[j];
-            diag = up;
-            uint32_t t = nwap_viaddmax_s16x2(up, sc.u2h, dw);
+            const uint32_t t = nwap_viaddmax_s16x2(P[j], sc.u2h, dw);
             cur = nwap_vmaxs2(t, left);
         }
         P[j] = cur;
         left = cur;
+        dw = dw_next;
+    }
+}
+
+// All la matrix rows of one row word; returns P[] holding matrix row la.
+template <int LB, int FLAVOR>
+NWAP_HD void nwap_dp_word(const uint32_t *row_sym2, int la, const uint32_t *nb,
+                          uint32_t (&P)[LB + 1], const nwap_scheme_consts &sc)
+{
+#pragma unroll
+    for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;        // H'[0][j]
+    uint32_t left0 = NWAP_BIAS2;                            // H'[0][0]
+#pragma unroll 1
+    for (int i = 0; i < la; ++i) {
+        const uint32_t d0 = left0;
+        left0 += sc.u2;                                     // H'[i+1][0]
+        nwap_dp_row<LB, FLAVOR>(row_sym2[i], nb, P, d0, left0, sc);
     }
 }
 
 // Whole pair-of-pairs DP for one row word; returns the packed H' values at
 // (la, lb0) in the low half and (la, lb1) in the high half.  Used by the host
-// emulation test and (unrolled differently) by the tile kernel.
+// emulation test; the tile kernel calls nwap_dp_word directly.
 template <int LB, int FLAVOR>
 NWAP_HD uint32_t nwap_dp_pair(const uint32_t *row_sym2, int la, const uint32_t (&nb)[LB],
                               int lb0, int lb1, const nwap_scheme_consts &sc)
 {
-    uint32_t P[LB + 1], PU[LB + 1];
-    uint32_t left0 = NWAP_BIAS2 + sc.u2;
-    nwap_dp_row<LB, FLAVOR, true>(row_sym2[0], nb, P, PU, left0, sc);
-    for (int i = 1; i < la; ++i) {
-        left0 += sc.u2;
-        nwap_dp_row<LB, FLAVOR, false>(row_sym2[i], nb, P, PU, left0, sc);
-    }
+    uint32_t P[LB + 1];
+    nwap_dp_word<LB, FLAVOR>(row_sym2, la, nb, P, sc);
     uint32_t lo = 0, hi = 0;
 #pragma unroll
     for (int j = 1; j <= LB; ++j) {

@@ -86,17 +86,41 @@ __device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
     return (w[j >> 2] >> (8 * (j & 3))) & 0xffu;
 }
 
+// One row word against the lane's two columns at register width LB; returns the packed
+// final cells (low half: column 0 of the lane, high half: column 1).
+template <int LB, int FLAVOR>
+__device__ __forceinline__ uint32_t nwap_row_vs_lane(const uint32_t *sym, int la, const uint32_t *nb,
+                                                     int l0, int l1, bool mixed,
+                                                     const nwap_scheme_consts &sc)
+{
+    uint32_t P[LB + 1];
+    nwap_dp_word<LB, FLAVOR>(sym, la, nb, P, sc);
+    uint32_t v = P[LB];
+    if (mixed) {                                     // warp-uniform, rare after the sort
+        uint32_t lo = v & 0xffffu, hi = v >> 16;
+#pragma unroll
+        for (int j = 1; j < LB; ++j) {
+            if (j == l0) lo = P[j] & 0xffffu;
+            if (j == l1) hi = P[j] >> 16;
+        }
+        v = lo | (hi << 16);
+    }
+    return v;
+}
+
 // One chunk (64 sorted columns, 2 per lane) against every staged row of the band.
-template <int LB, int FLAVOR, int QW>
-__device__ __forceinline__ void nwap_run_chunk(nwap_tile_smem &sm, const nwap_scheme_consts &sc,
+// The length-specialised code is only the DP itself (selected per row by a jump table);
+// score fix-up, staging store and statistics are shared by all lengths.
+template <int FLAVOR, int QMAX, int QW>
+__device__ __forceinline__ void nwap_run_chunk(int LB, nwap_tile_smem &sm, const nwap_scheme_consts &sc,
                                                const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
                                                int l0, int l1, uint32_t off0, uint32_t off1,
                                                bool mixed, int want_hist,
                                                int &tsum, int &tcnt, int &tmn, int &tmx)
 {
-    uint32_t nb[LB];
+    uint32_t nb[QMAX];
 #pragma unroll
-    for (int j = 0; j < LB; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
     const int k0 = sc.beta * l0 - (int)NWAP_BIAS;
     const int k1 = sc.beta * l1 - (int)NWAP_BIAS;
 
@@ -104,33 +128,23 @@ __device__ __forceinline__ void nwap_run_chunk(nwap_tile_smem &sm, const nwap_sc
     for (int rr = 0; rr < NWAP_R; ++rr) {
         const int la = sm.meta[rr].la;
         if (la == 0) continue;                       // uniform across the CTA
-        uint32_t P[LB + 1], PU[LB + 1];
-        uint32_t left0 = NWAP_BIAS2 + sc.u2;
         const uint32_t *sym = sm.rowsym[rr];
-        nwap_dp_row<LB, FLAVOR, true>(sym[0], nb, P, PU, left0, sc);
-        int i = 1;
-#pragma unroll 1
-        for (; i + 1 < la; i += 2) {                 // two matrix rows per trip: no register rotation moves
-            const uint32_t l1 = left0 + sc.u2;
-            left0 = l1 + sc.u2;
-            nwap_dp_row<LB, FLAVOR, false>(sym[i], nb, P, PU, l1, sc);
-            nwap_dp_row<LB, FLAVOR, false>(sym[i + 1], nb, P, PU, left0, sc);
+        uint32_t v = 0;
+#define NWAP_CASE(n)                                                                             \
+    case n:                                                                                      \
+        if (n <= QMAX) v = nwap_row_vs_lane<(n <= QMAX ? n : 1), FLAVOR>(sym, la, nb, l0, l1, mixed, sc); \
+        break;
+        switch (LB) {
+            NWAP_CASE(1) NWAP_CASE(2) NWAP_CASE(3) NWAP_CASE(4) NWAP_CASE(5) NWAP_CASE(6) NWAP_CASE(7) NWAP_CASE(8)
+            NWAP_CASE(9) NWAP_CASE(10) NWAP_CASE(11) NWAP_CASE(12) NWAP_CASE(13) NWAP_CASE(14) NWAP_CASE(15) NWAP_CASE(16)
+            NWAP_CASE(17) NWAP_CASE(18) NWAP_CASE(19) NWAP_CASE(20) NWAP_CASE(21) NWAP_CASE(22) NWAP_CASE(23) NWAP_CASE(24)
+            NWAP_CASE(25) NWAP_CASE(26) NWAP_CASE(27) NWAP_CASE(28) NWAP_CASE(29) NWAP_CASE(30) NWAP_CASE(31) NWAP_CASE(32)
+        default: break;
         }
-        if (i < la) {
-            left0 += sc.u2;
-            nwap_dp_row<LB, FLAVOR, false>(sym[i], nb, P, PU, left0, sc);
-        }
-        uint32_t lo = P[LB] & 0xffffu, hi = P[LB] >> 16;
-        if (mixed) {                                 // warp-uniform, rare after the sort
-#pragma unroll
-            for (int j = 1; j < LB; ++j) {
-                if (j == l0) lo = P[j] & 0xffffu;
-                if (j == l1) hi = P[j] >> 16;
-            }
-        }
+#undef NWAP_CASE
         const int ala = sm.meta[rr].alpha_la;
-        const int s0 = (int)lo + k0 + ala;
-        const int s1 = (int)hi + k1 + ala;
+        const int s0 = (int)(v & 0xffffu) + k0 + ala;
+        const int s1 = (int)(v >> 16) + k1 + ala;
         const uint32_t clo = (uint32_t)sm.meta[rr].clo_off;
         const uint32_t seg = (uint32_t)sm.meta[rr].seglen;
         const int adj = sm.meta[rr].rowadj;
@@ -147,39 +161,18 @@ __device__ __forceinline__ void nwap_run_chunk(nwap_tile_smem &sm, const nwap_sc
     }
 }
 
-template <int FLAVOR, int QW>
-__device__ __forceinline__ void nwap_dispatch_chunk(int LB, nwap_tile_smem &sm, const nwap_scheme_consts &sc,
-                                                    const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
-                                                    int l0, int l1, uint32_t off0, uint32_t off1,
-                                                    bool mixed, int want_hist,
-                                                    int &tsum, int &tcnt, int &tmn, int &tmx)
-{
-#define NWAP_CASE(n)                                                                              \
-    case n:                                                                                       \
-        if (n <= QW * 4)                                                                          \
-            nwap_run_chunk<(n <= QW * 4 ? n : 1), FLAVOR, QW>(sm, sc, w0, w1, l0, l1, off0, off1, \
-                                                              mixed, want_hist, tsum, tcnt, tmn, tmx); \
-        break;
-    switch (LB) {
-        NWAP_CASE(1) NWAP_CASE(2) NWAP_CASE(3) NWAP_CASE(4) NWAP_CASE(5) NWAP_CASE(6) NWAP_CASE(7) NWAP_CASE(8)
-        NWAP_CASE(9) NWAP_CASE(10) NWAP_CASE(11) NWAP_CASE(12) NWAP_CASE(13) NWAP_CASE(14) NWAP_CASE(15) NWAP_CASE(16)
-        NWAP_CASE(17) NWAP_CASE(18) NWAP_CASE(19) NWAP_CASE(20) NWAP_CASE(21) NWAP_CASE(22) NWAP_CASE(23) NWAP_CASE(24)
-        NWAP_CASE(25) NWAP_CASE(26) NWAP_CASE(27) NWAP_CASE(28) NWAP_CASE(29) NWAP_CASE(30) NWAP_CASE(31) NWAP_CASE(32)
-    default: break;
-    }
-#undef NWAP_CASE
-}
-
-// QW = words (4 symbols each) per stored word row: qpad/4 = 4 (q<=16) or 8 (q<=32).
-template <int FLAVOR, int QW>
-__global__ void __launch_bounds__(NWAP_THREADS)
+// QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
+// accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
+template <int FLAVOR, int QMAX>
+__global__ void __launch_bounds__(NWAP_THREADS, (QMAX <= 24 ? 5 : 4))
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     nwap_tile_smem &sm = *reinterpret_cast<nwap_tile_smem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const nwap_scheme_consts sc = p.sc;
-    constexpr int MAXL = QW * 4;
+    constexpr int MAXL = QMAX;
+    constexpr int QW = QMAX <= 16 ? 4 : 8;
 
     if (tid == 0) { sm.sum = 0; sm.count = 0; sm.mn = 127; sm.mx = -128; }
     for (int b = tid; b < 256; b += NWAP_THREADS) sm.hist[b] = 0;
@@ -312,7 +305,7 @@ k_score_tiles(const nwap_tile_params p)
                     w0[4 * v] = x.x; w0[4 * v + 1] = x.y; w0[4 * v + 2] = x.z; w0[4 * v + 3] = x.w;
                     w1[4 * v] = y.x; w1[4 * v + 1] = y.y; w1[4 * v + 2] = y.z; w1[4 * v + 3] = y.w;
                 }
-                nwap_dispatch_chunk<FLAVOR, QW>(LB, sm, sc, w0, w1, la_, lb_, off0, off1, mixed,
+                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, la_, lb_, off0, off1, mixed,
                                                 p.want_hist, tsum, tcnt, tmn, tmx);
             }
             __syncthreads();
@@ -623,8 +616,18 @@ __global__ void k_rows_cols(int64_t n, const int64_t *idx, int64_t count, int64_
 }
 
 // ---------------------------------------------------------------------------
-// Instruction-issue probes: 8 independent chains per thread, unrolled 16x.
+// Instruction-issue probes: 8 independent chains per thread, unrolled 16x, every
+// operation an `asm volatile` so nothing is folded.  See NWAP_PROBE_* in nwap.h.
 // ---------------------------------------------------------------------------
+#define NWAP_OP3(name, x, a, b) asm volatile(name " %0, %0, %1, %2;" : "+r"(x) : "r"(a), "r"(b))
+#define NWAP_OP2(name, x, a) asm volatile(name " %0, %0, %1;" : "+r"(x) : "r"(a))
+__device__ __forceinline__ void nwap_p_viaddmin(uint32_t &x, uint32_t a, uint32_t c)
+{ asm volatile("{.reg .b32 t; add.u16x2 t, %0, %1; min.u16x2 %0, t, %2;}" : "+r"(x) : "r"(a), "r"(c)); }
+__device__ __forceinline__ void nwap_p_vimax3(uint32_t &x, uint32_t a, uint32_t c)
+{ asm volatile("{.reg .b32 t; max.s16x2 t, %0, %1; max.s16x2 %0, t, %2;}" : "+r"(x) : "r"(a), "r"(c)); }
+__device__ __forceinline__ void nwap_p_imad(uint32_t &x, uint32_t a, uint32_t c)
+{ asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x) : "r"(a), "r"(c)); }
+
 template <int WHICH>
 __global__ void __launch_bounds__(512)
 k_probe(int iters, uint32_t a, uint32_t b, uint32_t c, uint32_t one, uint32_t *sink, long long *cycles)
@@ -640,25 +643,49 @@ k_probe(int iters, uint32_t a, uint32_t b, uint32_t c, uint32_t one, uint32_t *s
         for (int u = 0; u < 16; ++u) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                if (WHICH == 0) x[k] = __viaddmin_u16x2(x[k], b, c);
-                else if (WHICH == 1) x[k] = __vimax3_s16x2(x[k], b, y[k]);
-                else if (WHICH == 2) x[k] = __vmaxs2(x[k], y[k]);          // VIMNMX.S16x2
-                else if (WHICH == 3) x[k] = x[k] * a + b;                 // IMAD
-                else if (WHICH == 4) x[k] = (x[k] & b) ^ y[k];            // LOP3
-                else if (WHICH == 5) x[k] = x[k] + b + y[k];              // IADD3
-                else if (WHICH == 6) {                                    // 2 ALU + 2 IMAD cell
-                    const uint32_t e = __viaddmin_u16x2(a, y[k], 0x00010001u);
-                    const uint32_t dw = e * b + x[k];
-                    const uint32_t cur = __vimax3_s16x2(dw, y[k], x[k]);
-                    y[k] = cur * one + c;
-                    x[k] = cur;
-                } else {                                                  // 3 ALU + 1 IMAD cell
-                    const uint32_t e = __viaddmin_u16x2(a, y[k], 0x00010001u);
-                    const uint32_t dw = e * b + x[k];
-                    const uint32_t tt = __viaddmax_s16x2(y[k], c, dw);
-                    x[k] = __vmaxs2(tt, x[k]);
-                    y[k] = x[k];
+                if (WHICH == 0) nwap_p_viaddmin(x[k], b, c);
+                else if (WHICH == 1) nwap_p_vimax3(x[k], b, y[k]);
+                else if (WHICH == 2) NWAP_OP2("max.s16x2", x[k], y[k]);
+                else if (WHICH == 3) nwap_p_imad(x[k], a, b);
+                else if (WHICH == 4) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(b), "r"(y[k]));
+                else if (WHICH == 5) NWAP_OP2("add.u32", x[k], y[k]);
+                else if (WHICH == 6) {                                    // 2 DPX + 2 IMAD cell
+                    uint32_t e = a; nwap_p_viaddmin(e, y[k], 0x00010001u);
+                    nwap_p_imad(e, b, x[k]);
+                    nwap_p_vimax3(x[k], e, y[k]);
+                    y[k] = x[k]; nwap_p_imad(y[k], one, c);
+                } else if (WHICH == 7) {                                  // 3 DPX/ALU + 1 IMAD cell
+                    uint32_t e = a; nwap_p_viaddmin(e, y[k], 0x00010001u);
+                    nwap_p_imad(e, b, x[k]);
+                    asm volatile("{.reg .b32 t; add.s16x2 t, %0, %1; max.s16x2 %0, t, %2;}" : "+r"(y[k]) : "r"(c), "r"(e));
+                    NWAP_OP2("max.s16x2", x[k], y[k]);
                 }
+                else if (WHICH == 8) NWAP_OP2("add.u16x2", x[k], y[k]);
+                else if (WHICH == 9) NWAP_OP2("min.u16x2", x[k], y[k]);
+                else if (WHICH == 10) asm volatile("fma.rn.f16x2 %0, %0, %1, %2;" : "+r"(x[k]) : "r"(a), "r"(b));
+                else if (WHICH == 11) NWAP_OP2("max.f16x2", x[k], y[k]);
+                else if (WHICH == 12) asm volatile("prmt.b32 %0, %0, %1, %2;" : "+r"(x[k]) : "r"(y[k]), "r"(b));
+                else if (WHICH == 13) { nwap_p_vimax3(x[k], b, c); NWAP_OP2("add.u32", y[k], a); }          // DPX + IADD
+                else if (WHICH == 14) { nwap_p_vimax3(x[k], b, c); NWAP_OP2("max.s16x2", y[k], a); }        // DPX + VIMNMX2
+                else if (WHICH == 15) { nwap_p_imad(x[k], a, b); NWAP_OP2("add.u32", y[k], a); }            // IMAD + IADD
+                else if (WHICH == 16) { nwap_p_imad(x[k], a, b); asm volatile("fma.rn.f16x2 %0, %0, %1, %2;" : "+r"(y[k]) : "r"(a), "r"(b)); }
+                else if (WHICH == 17) { nwap_p_vimax3(x[k], b, c); nwap_p_imad(y[k], a, b); }               // DPX + IMAD
+                else if (WHICH == 18) {                                   // cell with IADD for up+u: 2 DPX + IMAD + IADD
+                    uint32_t e = a; nwap_p_viaddmin(e, y[k], 0x00010001u);
+                    nwap_p_imad(e, b, x[k]);
+                    nwap_p_vimax3(x[k], e, y[k]);
+                    y[k] = x[k]; NWAP_OP2("add.u32", y[k], c);
+                } else if (WHICH == 19) {                                 // cell with 2-input max: DPX + 2 IMAD + 2 VIMNMX2
+                    uint32_t e = a; nwap_p_viaddmin(e, y[k], 0x00010001u);
+                    nwap_p_imad(e, b, x[k]);
+                    NWAP_OP2("max.s16x2", x[k], e); NWAP_OP2("max.s16x2", x[k], y[k]);
+                    y[k] = x[k]; nwap_p_imad(y[k], one, c);
+                } else if (WHICH == 20) {                                 // cell: xor + min2 + IMAD + VIMNMX3 + IMAD
+                    uint32_t e = a; NWAP_OP2("xor.b32", e, y[k]); NWAP_OP2("min.u16x2", e, one);
+                    nwap_p_imad(e, b, x[k]);
+                    nwap_p_vimax3(x[k], e, y[k]);
+                    y[k] = x[k]; nwap_p_imad(y[k], one, c);
+                } else if (WHICH == 21) { nwap_p_viaddmin(x[k], b, c); nwap_p_vimax3(y[k], b, c); }         // two DPX kinds
             }
         }
     }
