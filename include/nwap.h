@@ -42,8 +42,8 @@ extern "C" {
 /* kernel variants selectable per call (nwap_score_range `variant`) */
 #define NWAP_VARIANT_AUTO    0  /* packed DPX tile kernel when the scheme/store allow it, else simple */
 #define NWAP_VARIANT_SIMPLE  1  /* one thread per pair, int32 cells, K x K table: any scheme, any q <= 255 */
-#define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 ALU + 2 IMAD per packed cell */
-#define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 3 ALU + 1 IMAD per packed cell */
+#define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 DPX + 2 IMAD per packed cell */
+#define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 2 DPX + 1 IMAD + 1 IADD per packed cell */
 
 typedef struct nwap_ctx nwap_ctx;
 

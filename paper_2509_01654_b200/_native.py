@@ -8,8 +8,11 @@ from pathlib import Path
 
 from .host_types import DataError
 
+import os
+
 _CSRC = Path(__file__).resolve().parent / "csrc"
-LIB_PATH = _CSRC / "libnwap.so"
+# NWAP_LIB selects an A/B build of the same sources (csrc/Makefile `variant` target)
+LIB_PATH = Path(os.environ["NWAP_LIB"]).resolve() if os.environ.get("NWAP_LIB") else _CSRC / "libnwap.so"
 
 NWAP_OK, NWAP_EINVAL, NWAP_ERANGE, NWAP_ECUDA, NWAP_ENOMEM, NWAP_ECAPACITY = 0, -1, -2, -3, -4, -5
 VARIANT_AUTO, VARIANT_SIMPLE, VARIANT_PACKED, VARIANT_PACKED3 = 0, 1, 2, 3

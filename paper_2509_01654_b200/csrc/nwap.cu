@@ -124,7 +124,8 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
 {
     if (start >= end) return NWAP_OK;
     const bool fast_ok = !c->general && c->qmax <= NWAP_MAXLEN_FAST;
-    if (variant == NWAP_VARIANT_AUTO) variant = fast_ok ? NWAP_VARIANT_PACKED : NWAP_VARIANT_SIMPLE;
+    // PACKED3 (2 DPX + IMAD + IADD) measured ~8 % faster than PACKED (2 DPX + 2 IMAD): profiles/r01_ab.txt
+    if (variant == NWAP_VARIANT_AUTO) variant = fast_ok ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
     if ((variant == NWAP_VARIANT_PACKED || variant == NWAP_VARIANT_PACKED3) && !fast_ok)
         return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme and max word length <= %d (have %d%s)",
                     NWAP_MAXLEN_FAST, c->qmax, c->general ? ", explicit similarity table" : "");

@@ -16,8 +16,10 @@
 //     dw  = IMAD            (e * (-D) + diag)        FMA pipe  (packed-safe: halves stay in [0,2^15))
 //     cur = VIMNMX3.S16x2   (dw, up_plus_u, left)    ALU pipe
 //     upu = IMAD            (cur * 1 + u*65537)      FMA pipe  (next row's up + u)
-// i.e. 2 ALU + 2 FMA-pipe issues (FLAVOR 0).  FLAVOR 1 folds the vertical add
-// into VIADDMNMX.S16x2 instead (3 ALU + 1 IMAD, one rolling array).
+// i.e. 2 DPX + 2 FMA-pipe issues (FLAVOR 0).  FLAVOR 1 forms up+u with a plain
+// 32-bit IADD instead (2 DPX + 1 IMAD + 1 IADD): on B200 the 3-input DPX ops and IMAD
+// are half-rate on separate pipes while IADD is full-rate and co-issues with both
+// (profiles/r01b_probes.txt).
 //
 // All halves stay inside [0, 2^15): |H| <= 128 by the int8 preflight
 // (engine.py:72-96), |(match-gap)*i| <= 192, |gap*j| <= 64, |D| <= 256, and
@@ -131,13 +133,9 @@ NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
         uint32_t dw_next = 0;
         if (j < LB) dw_next = nwap_viaddmin_u16x2(a2, nb[j], 0x00010001u) * sc.neg_delta + P[j];
         uint32_t cur;
-        if (FLAVOR == 0) {
-            const uint32_t upu = P[j] * sc.one + sc.u2;
-            cur = nwap_vimax3_s16x2(dw, upu, left);
-        } else {
-            const uint32_t t = nwap_viaddmax_s16x2(P[j], sc.u2h, dw);
-            cur = nwap_vmaxs2(t, left);
-        }
+        // up + u: halves stay in [0, 2^15), so a plain 32-bit add/IMAD of u*65537 is a packed add
+        const uint32_t upu = FLAVOR == 0 ? P[j] * sc.one + sc.u2 : P[j] + sc.u2;
+        cur = nwap_vimax3_s16x2(dw, upu, left);
         P[j] = cur;
         left = cur;
         dw = dw_next;
@@ -145,26 +143,65 @@ NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
 }
 
 // All la matrix rows of one row word; returns P[] holding matrix row la.
+// row_sym2[i] = {a_i * 65537, H'[i+1][0]}: the packed symbol of matrix row i+1 and that
+// row's boundary value (BIAS2 + (i+1)*u2, the same for every word), fetched together.
+struct nwap_sym2 { uint32_t a2, left0; };
+
+// Build-time micro-variants (A/B-tested on the GPU, see profiles/):
+//   NWAP_SYM64    1: fetch {symbol, boundary} with one 8-byte load; 0: load the symbol, add u2
+//   NWAP_PREFETCH 1: load the next matrix row's symbol before working on the current one
+#ifndef NWAP_SYM64
+#define NWAP_SYM64 1
+#endif
+#ifndef NWAP_PREFETCH
+#define NWAP_PREFETCH 0
+#endif
+
 template <int LB, int FLAVOR>
-NWAP_HD void nwap_dp_word(const uint32_t *row_sym2, int la, const uint32_t *nb,
+NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
                           uint32_t (&P)[LB + 1], const nwap_scheme_consts &sc)
 {
 #pragma unroll
     for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;        // H'[0][j]
-    uint32_t left0 = NWAP_BIAS2;                            // H'[0][0]
+    uint32_t d0 = NWAP_BIAS2;                               // H'[0][0]
+    const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
+#if NWAP_PREFETCH
+    nwap_sym2 x = *s;
 #pragma unroll 1
-    for (int i = 0; i < la; ++i) {
-        const uint32_t d0 = left0;
-        left0 += sc.u2;                                     // H'[i+1][0]
-        nwap_dp_row<LB, FLAVOR>(row_sym2[i], nb, P, d0, left0, sc);
-    }
+    do {                                                    // la >= 1 always
+        ++s;
+        const nwap_sym2 cur = x;
+        x = *s;                                             // one element past the word is readable padding
+#if NWAP_SYM64
+        const uint32_t left0 = cur.left0;
+#else
+        const uint32_t left0 = d0 + sc.u2;
+#endif
+        nwap_dp_row<LB, FLAVOR>(cur.a2, nb, P, d0, left0, sc);
+        d0 = left0;
+    } while (s != e);
+#else
+#pragma unroll 1
+    do {                                                    // la >= 1 always
+#if NWAP_SYM64
+        const nwap_sym2 x = *s++;
+        const uint32_t left0 = x.left0;
+        const uint32_t a2 = x.a2;
+#else
+        const uint32_t a2 = (s++)->a2;
+        const uint32_t left0 = d0 + sc.u2;
+#endif
+        nwap_dp_row<LB, FLAVOR>(a2, nb, P, d0, left0, sc);
+        d0 = left0;
+    } while (s != e);
+#endif
 }
 
 // Whole pair-of-pairs DP for one row word; returns the packed H' values at
 // (la, lb0) in the low half and (la, lb1) in the high half.  Used by the host
 // emulation test; the tile kernel calls nwap_dp_word directly.
 template <int LB, int FLAVOR>
-NWAP_HD uint32_t nwap_dp_pair(const uint32_t *row_sym2, int la, const uint32_t (&nb)[LB],
+NWAP_HD uint32_t nwap_dp_pair(const nwap_sym2 *row_sym2, int la, const uint32_t (&nb)[LB],
                               int lb0, int lb1, const nwap_scheme_consts &sc)
 {
     uint32_t P[LB + 1];

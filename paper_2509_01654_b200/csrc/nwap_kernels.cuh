@@ -21,9 +21,12 @@
 #include "nwap_core.cuh"
 #include "nwap_index.cuh"
 
+#ifndef NWAP_COLD_FAMILY
+#define NWAP_COLD_FAMILY 0
+#endif
 #define NWAP_THREADS 128                 // 4 warps per CTA
 #define NWAP_WARPS (NWAP_THREADS / 32)
-#define NWAP_PITCH (NWAP_C + 32)         // bytes per staged output row (multiple of 16)
+#define NWAP_PITCH (NWAP_C + 16)         // bytes per staged output row (multiple of 16)
 #define NWAP_MAXLEN_FAST 32              // register-resident row limit
 
 struct nwap_dev_stats {                   // same layout as nwap_stats
@@ -53,13 +56,13 @@ struct nwap_tile_params {
 };
 
 struct nwap_row_meta {
-    int la;        // row word length, 0 = row not in this launch / no valid column in this strip
-    int clo_off;   // first valid column, relative to the strip
-    int seglen;    // number of valid columns in this strip for this row
-    int rowadj;    // smem byte index of (column offset 0): rr*PITCH + skew - clo_off
-    int alpha_la;  // alpha * la
-    int skew;      // (global address of the segment) & 15
-    int64_t g0;    // out-relative byte offset of the segment
+    int la;            // row word length, 0 = row not in this launch / no valid column in this strip
+    uint32_t ala2;     // (alpha * la) * 65537: the row potential, packed for both halves
+    int clo_off;       // first valid column, relative to the strip
+    int seglen;        // number of valid columns in this strip for this row
+    int rowadj;        // smem byte index of (column offset 0): rr*PITCH + skew - clo_off
+    int skew;          // (global address of the segment) & 15
+    int64_t g0;        // out-relative byte offset of the segment
 };
 
 // ---------------------------------------------------------------------------
@@ -67,7 +70,7 @@ struct nwap_row_meta {
 // ---------------------------------------------------------------------------
 struct nwap_tile_smem {
     alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
-    alignas(16) uint32_t rowsym[NWAP_R][NWAP_MAXLEN_FAST];   // row symbols packed a*65537
+    alignas(16) nwap_sym2 rowsym[NWAP_R][NWAP_MAXLEN_FAST + 1];  // {a*65537, H'[i+1][0]} per matrix row (+1 pad)
     nwap_row_meta meta[NWAP_R];
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
     uint8_t clen[NWAP_C];         // their lengths
@@ -79,6 +82,7 @@ struct nwap_tile_smem {
     int mn, mx;
     int ncols;
     int next_chunk;
+    int band_simple;      // every staged row is valid over the whole sorted column window
 };
 
 __device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
@@ -86,80 +90,139 @@ __device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
     return (w[j >> 2] >> (8 * (j & 3))) & 0xffu;
 }
 
-// One row word against the lane's two columns at register width LB; returns the packed
-// final cells (low half: column 0 of the lane, high half: column 1).
-template <int LB, int FLAVOR>
-__device__ __forceinline__ uint32_t nwap_row_vs_lane(const uint32_t *sym, int la, const uint32_t *nb,
-                                                     int l0, int l1, bool mixed,
-                                                     const nwap_scheme_consts &sc)
+// Statistics are kept packed: t = H' + row potential + column potential has halves
+// score + BIAS, so min/max are one VIMNMX.S16x2 each for both pairs and the byte to store
+// is simply the low byte of each half (BIAS is a multiple of 256).
+struct nwap_lane_stats {
+    uint32_t mn2, mx2;      // packed running min / max of (score + BIAS)
+    long long sum;          // sum of scores
+    int count;              // valid pairs
+};
+
+// The only length-specialised code: the DP of one row word at register width LB.
+// HOT family (DEEP = false): returns the final cells for words of length LB (v) and LB-1
+// (vm1) -- all a sorted chunk normally contains.  COLD family (DEEP = true, a chunk spanning
+// three or more lengths: the long and short tails of a strip): full per-lane select.  The two
+// families are separate switch statements so the cold bodies stay out of the instruction cache.
+struct nwap_true { __device__ constexpr operator bool() const { return true; } };
+struct nwap_false { __device__ constexpr operator bool() const { return false; } };
+
+template <int LB, int FLAVOR, typename DeepT>
+__device__ __forceinline__ void nwap_row_dp(const nwap_sym2 *sym, int la, const uint32_t *nb, int l0, int l1,
+                                            const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1, DeepT DEEP)
 {
     uint32_t P[LB + 1];
     nwap_dp_word<LB, FLAVOR>(sym, la, nb, P, sc);
-    uint32_t v = P[LB];
-    if (mixed) {                                     // warp-uniform, rare after the sort
-        uint32_t lo = v & 0xffffu, hi = v >> 16;
+    v = P[LB];
+    vm1 = P[LB >= 2 ? LB - 1 : LB];
+    if (DEEP) {
+        uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
 #pragma unroll
         for (int j = 1; j < LB; ++j) {
             if (j == l0) lo = P[j] & 0xffffu;
-            if (j == l1) hi = P[j] >> 16;
+            if (j == l1) hi = P[j] & 0xffff0000u;
         }
-        v = lo | (hi << 16);
+        v = lo | hi;
     }
-    return v;
 }
 
+#define NWAP_DP_SWITCH(DEEPFLAG)                                                                          \
+    switch (LB) {                                                                                         \
+        NWAP_CASE(1, DEEPFLAG) NWAP_CASE(2, DEEPFLAG) NWAP_CASE(3, DEEPFLAG) NWAP_CASE(4, DEEPFLAG)       \
+        NWAP_CASE(5, DEEPFLAG) NWAP_CASE(6, DEEPFLAG) NWAP_CASE(7, DEEPFLAG) NWAP_CASE(8, DEEPFLAG)       \
+        NWAP_CASE(9, DEEPFLAG) NWAP_CASE(10, DEEPFLAG) NWAP_CASE(11, DEEPFLAG) NWAP_CASE(12, DEEPFLAG)    \
+        NWAP_CASE(13, DEEPFLAG) NWAP_CASE(14, DEEPFLAG) NWAP_CASE(15, DEEPFLAG) NWAP_CASE(16, DEEPFLAG)   \
+        NWAP_CASE(17, DEEPFLAG) NWAP_CASE(18, DEEPFLAG) NWAP_CASE(19, DEEPFLAG) NWAP_CASE(20, DEEPFLAG)   \
+        NWAP_CASE(21, DEEPFLAG) NWAP_CASE(22, DEEPFLAG) NWAP_CASE(23, DEEPFLAG) NWAP_CASE(24, DEEPFLAG)   \
+        NWAP_CASE(25, DEEPFLAG) NWAP_CASE(26, DEEPFLAG) NWAP_CASE(27, DEEPFLAG) NWAP_CASE(28, DEEPFLAG)   \
+        NWAP_CASE(29, DEEPFLAG) NWAP_CASE(30, DEEPFLAG) NWAP_CASE(31, DEEPFLAG) NWAP_CASE(32, DEEPFLAG)   \
+    default: break;                                                                                       \
+    }
+#define NWAP_CASE(n, DEEPFLAG)                                                                            \
+    case n:                                                                                               \
+        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, la, nb, l0, l1, sc, v, vm1, DEEPFLAG); \
+        break;
+
 // One chunk (64 sorted columns, 2 per lane) against every staged row of the band.
-// The length-specialised code is only the DP itself (selected per row by a jump table);
-// score fix-up, staging store and statistics are shared by all lengths.
+// mixmode: 0 = every lane of the warp has both words of length LB; 1 = some are LB-1 (the
+// usual case at a bucket boundary of the sorted strip); 2 = anything.  fast: the chunk is full
+// and every staged row is valid over the whole column window, so no per-lane range checks are
+// needed (the overwhelmingly common case).  All warp-uniform.
 template <int FLAVOR, int QMAX, int QW>
 __device__ __forceinline__ void nwap_run_chunk(int LB, nwap_tile_smem &sm, const nwap_scheme_consts &sc,
                                                const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
                                                int l0, int l1, uint32_t off0, uint32_t off1,
-                                               bool mixed, int want_hist,
-                                               int &tsum, int &tcnt, int &tmn, int &tmx)
+                                               int mixmode, bool fast, int want_hist, nwap_lane_stats &ls)
 {
     uint32_t nb[QMAX];
 #pragma unroll
     for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
-    const int k0 = sc.beta * l0 - (int)NWAP_BIAS;
-    const int k1 = sc.beta * l1 - (int)NWAP_BIAS;
-
+    // column potentials, packed; the BIAS stays in (halves of t are score + BIAS)
+    const uint32_t kpos2 = (uint32_t)(sc.beta * l0) + ((uint32_t)(sc.beta * l1) << 16);
+    // per-lane masks selecting v (length LB) or vm1 (length LB-1) for each half
+    const uint32_t keep_v = (l0 == LB ? 0xffffu : 0u) | (l1 == LB ? 0xffff0000u : 0u);
+    uint32_t acc = 0, acc_hi = 0;     // per-chunk packed sums of t (<= 16 rows: no overflow)
+    int rows_fast = 0;
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
-        const int la = sm.meta[rr].la;
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
         if (la == 0) continue;                       // uniform across the CTA
-        const uint32_t *sym = sm.rowsym[rr];
-        uint32_t v = 0;
-#define NWAP_CASE(n)                                                                             \
-    case n:                                                                                      \
-        if (n <= QMAX) v = nwap_row_vs_lane<(n <= QMAX ? n : 1), FLAVOR>(sym, la, nb, l0, l1, mixed, sc); \
-        break;
-        switch (LB) {
-            NWAP_CASE(1) NWAP_CASE(2) NWAP_CASE(3) NWAP_CASE(4) NWAP_CASE(5) NWAP_CASE(6) NWAP_CASE(7) NWAP_CASE(8)
-            NWAP_CASE(9) NWAP_CASE(10) NWAP_CASE(11) NWAP_CASE(12) NWAP_CASE(13) NWAP_CASE(14) NWAP_CASE(15) NWAP_CASE(16)
-            NWAP_CASE(17) NWAP_CASE(18) NWAP_CASE(19) NWAP_CASE(20) NWAP_CASE(21) NWAP_CASE(22) NWAP_CASE(23) NWAP_CASE(24)
-            NWAP_CASE(25) NWAP_CASE(26) NWAP_CASE(27) NWAP_CASE(28) NWAP_CASE(29) NWAP_CASE(30) NWAP_CASE(31) NWAP_CASE(32)
-        default: break;
+        const nwap_sym2 *sym = sm.rowsym[rr];
+        uint32_t v = 0, vm1 = 0;
+#if NWAP_COLD_FAMILY
+        if (mixmode < 2) {
+            NWAP_DP_SWITCH(nwap_false())
+            if (mixmode) v = (v & keep_v) | (vm1 & ~keep_v);
+        } else {
+            NWAP_DP_SWITCH(nwap_true())
         }
-#undef NWAP_CASE
-        const int ala = sm.meta[rr].alpha_la;
-        const int s0 = (int)(v & 0xffffu) + k0 + ala;
-        const int s1 = (int)(v >> 16) + k1 + ala;
-        const uint32_t clo = (uint32_t)sm.meta[rr].clo_off;
-        const uint32_t seg = (uint32_t)sm.meta[rr].seglen;
-        const int adj = sm.meta[rr].rowadj;
-        if (off0 - clo < seg) {
-            sm.out[adj + (int)off0] = (uint8_t)(int8_t)s0;
-            tsum += s0; tcnt += 1; tmn = min(tmn, s0); tmx = max(tmx, s0);
-            if (want_hist) atomicAdd(&sm.hist[(s0 + 128) & 255], 1u);
-        }
-        if (off1 - clo < seg) {
-            sm.out[adj + (int)off1] = (uint8_t)(int8_t)s1;
-            tsum += s1; tcnt += 1; tmn = min(tmn, s1); tmx = max(tmx, s1);
-            if (want_hist) atomicAdd(&sm.hist[(s1 + 128) & 255], 1u);
+#else
+        const bool deep = mixmode > 1;               // full select inlined in every length body
+        NWAP_DP_SWITCH(deep)
+        if (mixmode == 1) v = (v & keep_v) | (vm1 & ~keep_v);
+#endif
+        const uint32_t t = v + m.ala2 + kpos2;       // halves: score + BIAS (never negative)
+        const uint32_t thi = t >> 16;
+        const int adj = m.rowadj;
+        if (fast) {
+            sm.out[adj + (int)off0] = (uint8_t)t;
+            sm.out[adj + (int)off1] = (uint8_t)thi;
+            ls.mn2 = __vmins2(ls.mn2, t);
+            ls.mx2 = __vmaxs2(ls.mx2, t);
+            acc += t;
+            acc_hi += thi;
+            ++rows_fast;
+        } else {
+            const uint32_t clo = (uint32_t)m.clo_off;
+            const uint32_t seg = (uint32_t)m.seglen;
+            const int s0 = (int)(t & 0xffffu) - (int)NWAP_BIAS;
+            const int s1 = (int)thi - (int)NWAP_BIAS;
+            if (off0 - clo < seg) {
+                sm.out[adj + (int)off0] = (uint8_t)(int8_t)s0;
+                ls.sum += s0; ls.count += 1;
+                ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffff0000u) | (t & 0xffffu));
+                ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffff0000u) | (t & 0xffffu));
+                if (want_hist) atomicAdd(&sm.hist[(s0 + 128) & 255], 1u);
+            }
+            if (off1 - clo < seg) {
+                sm.out[adj + (int)off1] = (uint8_t)(int8_t)s1;
+                ls.sum += s1; ls.count += 1;
+                ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffffu) | (t & 0xffff0000u));
+                ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffffu) | (t & 0xffff0000u));
+                if (want_hist) atomicAdd(&sm.hist[(s1 + 128) & 255], 1u);
+            }
         }
     }
+    if (rows_fast) {
+        // acc = sum(lo) + 65536 * sum(hi) (mod 2^32), acc_hi = sum(hi): both sums < 2^18
+        const uint32_t sum_lo = acc - (acc_hi << 16);
+        ls.sum += (long long)sum_lo + (long long)acc_hi - 2ll * rows_fast * (long long)NWAP_BIAS;
+        ls.count += 2 * rows_fast;
+    }
 }
+#undef NWAP_CASE
+#undef NWAP_DP_SWITCH
 
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
 // accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
@@ -176,7 +239,8 @@ k_score_tiles(const nwap_tile_params p)
 
     if (tid == 0) { sm.sum = 0; sm.count = 0; sm.mn = 127; sm.mx = -128; }
     for (int b = tid; b < 256; b += NWAP_THREADS) sm.hist[b] = 0;
-    int tsum = 0, tcnt = 0, tmn = 127, tmx = -128;
+    nwap_lane_stats ls;
+    ls.mn2 = 0x7fff7fffu; ls.mx2 = 0u; ls.sum = 0; ls.count = 0;
 
     for (;;) {
         __syncthreads();
@@ -248,7 +312,7 @@ k_score_tiles(const nwap_tile_params p)
             if (tid < NWAP_R) {
                 const int64_t r = rb0 + tid;
                 nwap_row_meta m;
-                m.la = 0; m.clo_off = 0; m.seglen = 0; m.rowadj = 0; m.alpha_la = 0; m.skew = 0; m.g0 = 0;
+                m.la = 0; m.clo_off = 0; m.seglen = 0; m.rowadj = 0; m.ala2 = 0; m.skew = 0; m.g0 = 0;
                 if (r >= rmin && r <= rmax) {
                     int64_t clo = max(strip_lo, r + 1);
                     int64_t chi = strip_hi;
@@ -261,7 +325,7 @@ k_score_tiles(const nwap_tile_params p)
                         m.g0 = nwap_before_row(r, p.n) + (clo - r - 1) - p.start;
                         m.skew = (int)((reinterpret_cast<uintptr_t>(p.out) + (uintptr_t)m.g0) & 15u);
                         m.rowadj = tid * NWAP_PITCH + m.skew - m.clo_off;
-                        m.alpha_la = sc.alpha * m.la;
+                        m.ala2 = (uint32_t)(sc.alpha * m.la * 65537);
                     }
                 }
                 sm.meta[tid] = m;
@@ -273,14 +337,29 @@ k_score_tiles(const nwap_tile_params p)
                 if (rr < NWAP_R && q4 < QW && r >= rmin && r <= rmax) {
                     const uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(p.ids + r * p.qpad) + q4);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) sm.rowsym[rr][q4 * 4 + e] = ((v >> (8 * e)) & 0xffu) * 65537u;
+                    for (int e = 0; e < 4; ++e) {
+                        nwap_sym2 x;
+                        x.a2 = ((v >> (8 * e)) & 0xffu) * 65537u;
+                        x.left0 = NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2;
+                        sm.rowsym[rr][q4 * 4 + e] = x;
+                    }
                 }
             }
             if (tid == 0) sm.next_chunk = 0;
             __syncthreads();
+            if (tid == 0) {
+                // simple band: all R rows present and each covers the whole sorted column window
+                int simple = !p.want_hist;
+                for (int rr = 0; rr < NWAP_R; ++rr)
+                    simple &= (sm.meta[rr].la > 0) && (sm.meta[rr].clo_off <= win_lo) &&
+                              (sm.meta[rr].clo_off + sm.meta[rr].seglen >= win_hi);
+                sm.band_simple = simple;
+            }
+            __syncthreads();
 
             // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
             const int ncols = sm.ncols;
+            const bool band_simple = sm.band_simple != 0;
             for (;;) {
                 int ch = 0;
                 if (lane == 0) ch = atomicAdd(&sm.next_chunk, 1);
@@ -293,7 +372,10 @@ k_score_tiles(const nwap_tile_params p)
                 const int la_ = va ? (int)sm.clen[ka] : LB, lb_ = vb ? (int)sm.clen[kb] : LB;
                 const uint32_t off0 = va ? (uint32_t)sm.cols[ka] : 0xffffu;
                 const uint32_t off1 = vb ? (uint32_t)sm.cols[kb] : 0xffffu;
-                const bool mixed = __any_sync(0xffffffffu, (la_ != LB) || (lb_ != LB));
+                const int lmin = min(la_, lb_);
+                const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
+                                  : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
+                const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
                 // column words (invalid lanes re-read the chunk's first column; their results are dropped)
                 const int64_t ca = strip_lo + (va ? sm.cols[ka] : sm.cols[kc]);
                 const int64_t cb = strip_lo + (vb ? sm.cols[kb] : sm.cols[kc]);
@@ -305,8 +387,8 @@ k_score_tiles(const nwap_tile_params p)
                     w0[4 * v] = x.x; w0[4 * v + 1] = x.y; w0[4 * v + 2] = x.z; w0[4 * v + 3] = x.w;
                     w1[4 * v] = y.x; w1[4 * v + 1] = y.y; w1[4 * v + 2] = y.z; w1[4 * v + 3] = y.w;
                 }
-                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, la_, lb_, off0, off1, mixed,
-                                                p.want_hist, tsum, tcnt, tmn, tmx);
+                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, la_, lb_, off0, off1, mixmode, fast,
+                                                 p.want_hist, ls);
             }
             __syncthreads();
 
@@ -331,7 +413,11 @@ k_score_tiles(const nwap_tile_params p)
     }
 
     // ---- statistics: thread -> warp -> CTA -> global ----
-    long long wsum = tsum, wcnt = tcnt;
+    long long wsum = ls.sum, wcnt = ls.count;
+    int tmn = min((int)(ls.mn2 & 0xffffu), (int)(ls.mn2 >> 16)) - (int)NWAP_BIAS;
+    int tmx = max((int)(ls.mx2 & 0xffffu), (int)(ls.mx2 >> 16)) - (int)NWAP_BIAS;
+    if (ls.count == 0) { tmn = 127; tmx = -128; }
+    tmn = min(tmn, 127); tmx = max(tmx, -128);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         wsum += __shfl_xor_sync(0xffffffffu, wsum, o);

@@ -10,8 +10,11 @@ template <int LB, int FLAVOR>
 static uint32_t run_pair(const uint8_t *a, int la, const uint8_t *b0, int lb0,
                          const uint8_t *b1, int lb1, const nwap_scheme_consts &sc)
 {
-    uint32_t row2[256];
-    for (int i = 0; i < la; ++i) row2[i] = (uint32_t)a[i] * 65537u;
+    nwap_sym2 row2[256];
+    for (int i = 0; i < la; ++i) {
+        row2[i].a2 = (uint32_t)a[i] * 65537u;
+        row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+    }
     uint32_t nb[LB];
     for (int j = 0; j < LB; ++j)
         nb[j] = nwap_pack_negb(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
