@@ -174,7 +174,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
         const int64_t g0 = p.r_first / rows_per_group, g1 = p.r_last / rows_per_group;
         ubeg = nwap_units_before_group(us, g0);
         ucount = nwap_units_before_group(us, g1 + 1) - ubeg;
-        if (gb == 1 || ucount >= slots * 24) break;
+        if (gb == 1 || ucount >= slots * NWAP_UNITS_PER_SLOT) break;
     }
     p.us = us; p.unit_begin = ubeg; p.unit_count = ucount;
     const int64_t grid = std::min<int64_t>(slots, ucount);

@@ -197,6 +197,56 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
 #endif
 }
 
+// ---- dual chain: the same row word against TWO column pairs per lane (registers PA/PB) ----
+// Halves the per-matrix-row loop overhead and the per-row dispatch for short words; the two
+// chains are independent, which also doubles the ILP of the max-chain.
+template <int LB, int FLAVOR>
+NWAP_HD void nwap_dp_row2(uint32_t a2, const uint32_t *nbA, const uint32_t *nbB,
+                          uint32_t (&PA)[LB + 1], uint32_t (&PB)[LB + 1],
+                          uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc)
+{
+    uint32_t leftA = left0, leftB = left0;
+    uint32_t dwA = nwap_viaddmin_u16x2(a2, nbA[0], 0x00010001u) * sc.neg_delta + d0;
+    uint32_t dwB = nwap_viaddmin_u16x2(a2, nbB[0], 0x00010001u) * sc.neg_delta + d0;
+#pragma unroll
+    for (int j = 1; j <= LB; ++j) {
+        uint32_t dwA_next = 0, dwB_next = 0;
+        if (j < LB) {
+            dwA_next = nwap_viaddmin_u16x2(a2, nbA[j], 0x00010001u) * sc.neg_delta + PA[j];
+            dwB_next = nwap_viaddmin_u16x2(a2, nbB[j], 0x00010001u) * sc.neg_delta + PB[j];
+        }
+        const uint32_t upuA = FLAVOR == 0 ? PA[j] * sc.one + sc.u2 : PA[j] + sc.u2;
+        const uint32_t upuB = FLAVOR == 0 ? PB[j] * sc.one + sc.u2 : PB[j] + sc.u2;
+        PA[j] = nwap_vimax3_s16x2(dwA, upuA, leftA);
+        PB[j] = nwap_vimax3_s16x2(dwB, upuB, leftB);
+        leftA = PA[j]; leftB = PB[j];
+        dwA = dwA_next; dwB = dwB_next;
+    }
+}
+
+template <int LB, int FLAVOR>
+NWAP_HD void nwap_dp_word2(const nwap_sym2 *row_sym2, int la, const uint32_t *nbA, const uint32_t *nbB,
+                           uint32_t (&PA)[LB + 1], uint32_t (&PB)[LB + 1], const nwap_scheme_consts &sc)
+{
+#pragma unroll
+    for (int j = 0; j <= LB; ++j) { PA[j] = NWAP_BIAS2; PB[j] = NWAP_BIAS2; }
+    uint32_t d0 = NWAP_BIAS2;
+    const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
+#pragma unroll 1
+    do {
+#if NWAP_SYM64
+        const nwap_sym2 x = *s++;
+        const uint32_t left0 = x.left0;
+        const uint32_t a2 = x.a2;
+#else
+        const uint32_t a2 = (s++)->a2;
+        const uint32_t left0 = d0 + sc.u2;
+#endif
+        nwap_dp_row2<LB, FLAVOR>(a2, nbA, nbB, PA, PB, d0, left0, sc);
+        d0 = left0;
+    } while (s != e);
+}
+
 // Whole pair-of-pairs DP for one row word; returns the packed H' values at
 // (la, lb0) in the low half and (la, lb1) in the high half.  Used by the host
 // emulation test; the tile kernel calls nwap_dp_word directly.
@@ -213,6 +263,25 @@ NWAP_HD uint32_t nwap_dp_pair(const nwap_sym2 *row_sym2, int la, const uint32_t 
         if (j == lb1) hi = P[j] >> 16;
     }
     return lo | (hi << 16);
+}
+
+// Dual-chain counterpart of nwap_dp_pair (host emulation test): four column words.
+template <int LB, int FLAVOR>
+NWAP_HD void nwap_dp_quad(const nwap_sym2 *row_sym2, int la, const uint32_t (&nbA)[LB], const uint32_t (&nbB)[LB],
+                          const int (&lens)[4], const nwap_scheme_consts &sc, uint32_t &outA, uint32_t &outB)
+{
+    uint32_t PA[LB + 1], PB[LB + 1];
+    nwap_dp_word2<LB, FLAVOR>(row_sym2, la, nbA, nbB, PA, PB, sc);
+    uint32_t a_lo = 0, a_hi = 0, b_lo = 0, b_hi = 0;
+#pragma unroll
+    for (int j = 1; j <= LB; ++j) {
+        if (j == lens[0]) a_lo = PA[j] & 0xffffu;
+        if (j == lens[1]) a_hi = PA[j] >> 16;
+        if (j == lens[2]) b_lo = PB[j] & 0xffffu;
+        if (j == lens[3]) b_hi = PB[j] >> 16;
+    }
+    outA = a_lo | (a_hi << 16);
+    outB = b_lo | (b_hi << 16);
 }
 
 // H'[la][lb] (one half, biased) -> true score.

@@ -20,8 +20,13 @@
 #endif
 
 // Tile geometry (compile-time): a band is R rows, a strip is C columns.
+#ifndef NWAP_THREADS
+#define NWAP_THREADS 128       // threads per CTA of the tile kernel
+#endif
+#ifndef NWAP_R
 #define NWAP_R 16
-#define NWAP_C 2048
+#endif
+#define NWAP_C (16 * NWAP_THREADS)   // one aligned uint4 of lengths per thread: 2048 columns
 #define NWAP_CHUNK 64          // sorted columns per warp chunk (2 per lane)
 
 NWAP_HD int64_t nwap_before_row(int64_t r, int64_t n) { return (r * (2 * n - r - 1)) >> 1; }

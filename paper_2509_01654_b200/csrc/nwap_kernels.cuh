@@ -24,7 +24,12 @@
 #ifndef NWAP_COLD_FAMILY
 #define NWAP_COLD_FAMILY 0
 #endif
-#define NWAP_THREADS 128                 // 4 warps per CTA
+#ifndef NWAP_MINB
+#define NWAP_MINB 5               // resident CTAs/SM the register allocator must allow (Q <= 24)
+#endif
+#ifndef NWAP_UNITS_PER_SLOT
+#define NWAP_UNITS_PER_SLOT 24
+#endif
 #define NWAP_WARPS (NWAP_THREADS / 32)
 #define NWAP_PITCH (NWAP_C + 16)         // bytes per staged output row (multiple of 16)
 #define NWAP_MAXLEN_FAST 32              // register-resident row limit
@@ -83,6 +88,7 @@ struct nwap_tile_smem {
     int ncols;
     int next_chunk;
     int band_simple;      // every staged row is valid over the whole sorted column window
+    int n_long_chunks;    // leading 64-column chunks that hold words longer than NWAP_DUAL_MAX
 };
 
 __device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
@@ -99,23 +105,91 @@ struct nwap_lane_stats {
     int count;              // valid pairs
 };
 
-// The only length-specialised code: the DP of one row word at register width LB.
-// HOT family (DEEP = false): returns the final cells for words of length LB (v) and LB-1
-// (vm1) -- all a sorted chunk normally contains.  COLD family (DEEP = true, a chunk spanning
-// three or more lengths: the long and short tails of a strip): full per-lane select.  The two
-// families are separate switch statements so the cold bodies stay out of the instruction cache.
+// One lane's two columns of a 64-column chunk.
+struct nwap_lane_cols {
+    uint32_t off0, off1;    // strip-relative column offsets (0xffff = no column)
+    int l0, l1;             // word lengths
+    uint32_t kpos2;         // column potentials, packed (BIAS stays in: halves of t are score + BIAS)
+    uint32_t keep_v;        // per-half mask: 0xffff where the word has length LB (else LB-1 in mixmode 1)
+};
+
+__device__ __forceinline__ nwap_lane_cols nwap_make_lane_cols(uint32_t off0, uint32_t off1, int l0, int l1, int LB,
+                                                              const nwap_scheme_consts &sc)
+{
+    nwap_lane_cols c;
+    c.off0 = off0; c.off1 = off1; c.l0 = l0; c.l1 = l1;
+    c.kpos2 = (uint32_t)(sc.beta * l0) + ((uint32_t)(sc.beta * l1) << 16);
+    c.keep_v = (l0 == LB ? 0xffffu : 0u) | (l1 == LB ? 0xffff0000u : 0u);
+    return c;
+}
+
+// Per-chunk packed accumulators of t (<= 2 * 16 rows: no overflow of either half-sum).
+struct nwap_chunk_acc { uint32_t acc, acc_hi; int rows_fast; };
+
+// Score fix-up, staging store and statistics of one packed result (shared by all lengths).
+__device__ __forceinline__ void nwap_emit(nwap_tile_smem &sm, const nwap_row_meta &m, uint32_t v,
+                                          const nwap_lane_cols &c, bool fast, int want_hist,
+                                          nwap_lane_stats &ls, nwap_chunk_acc &ca)
+{
+    const uint32_t t = v + m.ala2 + c.kpos2;        // halves: score + BIAS (never negative)
+    const uint32_t thi = t >> 16;
+    const int adj = m.rowadj;
+    if (fast) {
+        sm.out[adj + (int)c.off0] = (uint8_t)t;
+        sm.out[adj + (int)c.off1] = (uint8_t)thi;
+        ls.mn2 = __vmins2(ls.mn2, t);
+        ls.mx2 = __vmaxs2(ls.mx2, t);
+        ca.acc += t;
+        ca.acc_hi += thi;
+        ++ca.rows_fast;
+    } else {
+        const uint32_t clo = (uint32_t)m.clo_off;
+        const uint32_t seg = (uint32_t)m.seglen;
+        const int s0 = (int)(t & 0xffffu) - (int)NWAP_BIAS;
+        const int s1 = (int)thi - (int)NWAP_BIAS;
+        if (c.off0 - clo < seg) {
+            sm.out[adj + (int)c.off0] = (uint8_t)(int8_t)s0;
+            ls.sum += s0; ls.count += 1;
+            ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffff0000u) | (t & 0xffffu));
+            ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffff0000u) | (t & 0xffffu));
+            if (want_hist) atomicAdd(&sm.hist[(s0 + 128) & 255], 1u);
+        }
+        if (c.off1 - clo < seg) {
+            sm.out[adj + (int)c.off1] = (uint8_t)(int8_t)s1;
+            ls.sum += s1; ls.count += 1;
+            ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffffu) | (t & 0xffff0000u));
+            ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffffu) | (t & 0xffff0000u));
+            if (want_hist) atomicAdd(&sm.hist[(s1 + 128) & 255], 1u);
+        }
+    }
+}
+
+__device__ __forceinline__ void nwap_close_chunk(nwap_lane_stats &ls, const nwap_chunk_acc &ca)
+{
+    if (ca.rows_fast) {
+        // acc = sum(lo) + 65536 * sum(hi) (mod 2^32), acc_hi = sum(hi): both sums < 2^19
+        const uint32_t sum_lo = ca.acc - (ca.acc_hi << 16);
+        ls.sum += (long long)sum_lo + (long long)ca.acc_hi - 2ll * ca.rows_fast * (long long)NWAP_BIAS;
+        ls.count += 2 * ca.rows_fast;
+    }
+}
+
 struct nwap_true { __device__ constexpr operator bool() const { return true; } };
 struct nwap_false { __device__ constexpr operator bool() const { return false; } };
 
-template <int LB, int FLAVOR, typename DeepT>
+// The only length-specialised code: the DP of one row word at register width LB.  Returns the
+// final cells for words of length LB (v) and LB-1 (vm1) -- all a sorted chunk normally
+// contains; `deep` (a chunk spanning three or more lengths: the long and short tails of a
+// strip) selects per lane among all columns.
+template <int LB, int FLAVOR>
 __device__ __forceinline__ void nwap_row_dp(const nwap_sym2 *sym, int la, const uint32_t *nb, int l0, int l1,
-                                            const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1, DeepT DEEP)
+                                            const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1, bool deep)
 {
     uint32_t P[LB + 1];
     nwap_dp_word<LB, FLAVOR>(sym, la, nb, P, sc);
     v = P[LB];
     vm1 = P[LB >= 2 ? LB - 1 : LB];
-    if (DEEP) {
+    if (deep) {
         uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
 #pragma unroll
         for (int j = 1; j < LB; ++j) {
@@ -126,22 +200,35 @@ __device__ __forceinline__ void nwap_row_dp(const nwap_sym2 *sym, int la, const 
     }
 }
 
-#define NWAP_DP_SWITCH(DEEPFLAG)                                                                          \
-    switch (LB) {                                                                                         \
-        NWAP_CASE(1, DEEPFLAG) NWAP_CASE(2, DEEPFLAG) NWAP_CASE(3, DEEPFLAG) NWAP_CASE(4, DEEPFLAG)       \
-        NWAP_CASE(5, DEEPFLAG) NWAP_CASE(6, DEEPFLAG) NWAP_CASE(7, DEEPFLAG) NWAP_CASE(8, DEEPFLAG)       \
-        NWAP_CASE(9, DEEPFLAG) NWAP_CASE(10, DEEPFLAG) NWAP_CASE(11, DEEPFLAG) NWAP_CASE(12, DEEPFLAG)    \
-        NWAP_CASE(13, DEEPFLAG) NWAP_CASE(14, DEEPFLAG) NWAP_CASE(15, DEEPFLAG) NWAP_CASE(16, DEEPFLAG)   \
-        NWAP_CASE(17, DEEPFLAG) NWAP_CASE(18, DEEPFLAG) NWAP_CASE(19, DEEPFLAG) NWAP_CASE(20, DEEPFLAG)   \
-        NWAP_CASE(21, DEEPFLAG) NWAP_CASE(22, DEEPFLAG) NWAP_CASE(23, DEEPFLAG) NWAP_CASE(24, DEEPFLAG)   \
-        NWAP_CASE(25, DEEPFLAG) NWAP_CASE(26, DEEPFLAG) NWAP_CASE(27, DEEPFLAG) NWAP_CASE(28, DEEPFLAG)   \
-        NWAP_CASE(29, DEEPFLAG) NWAP_CASE(30, DEEPFLAG) NWAP_CASE(31, DEEPFLAG) NWAP_CASE(32, DEEPFLAG)   \
-    default: break;                                                                                       \
+// Dual chain: two column pairs per lane (A and B), same row word.
+template <int LB, int FLAVOR>
+__device__ __forceinline__ void nwap_row_dp2(const nwap_sym2 *sym, int la, const uint32_t *nbA, const uint32_t *nbB,
+                                             const nwap_lane_cols &cA, const nwap_lane_cols &cB,
+                                             const nwap_scheme_consts &sc, uint32_t &vA, uint32_t &vAm1,
+                                             uint32_t &vB, uint32_t &vBm1, bool deep)
+{
+    uint32_t PA[LB + 1], PB[LB + 1];
+    nwap_dp_word2<LB, FLAVOR>(sym, la, nbA, nbB, PA, PB, sc);
+    vA = PA[LB]; vB = PB[LB];
+    vAm1 = PA[LB >= 2 ? LB - 1 : LB]; vBm1 = PB[LB >= 2 ? LB - 1 : LB];
+    if (deep) {
+        uint32_t alo = vA & 0xffffu, ahi = vA & 0xffff0000u, blo = vB & 0xffffu, bhi = vB & 0xffff0000u;
+#pragma unroll
+        for (int j = 1; j < LB; ++j) {
+            if (j == cA.l0) alo = PA[j] & 0xffffu;
+            if (j == cA.l1) ahi = PA[j] & 0xffff0000u;
+            if (j == cB.l0) blo = PB[j] & 0xffffu;
+            if (j == cB.l1) bhi = PB[j] & 0xffff0000u;
+        }
+        vA = alo | ahi; vB = blo | bhi;
     }
-#define NWAP_CASE(n, DEEPFLAG)                                                                            \
-    case n:                                                                                               \
-        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, la, nb, l0, l1, sc, v, vm1, DEEPFLAG); \
-        break;
+}
+
+#define NWAP_CASES_1_32                                                                        \
+    NWAP_CASE(1) NWAP_CASE(2) NWAP_CASE(3) NWAP_CASE(4) NWAP_CASE(5) NWAP_CASE(6) NWAP_CASE(7) NWAP_CASE(8)         \
+    NWAP_CASE(9) NWAP_CASE(10) NWAP_CASE(11) NWAP_CASE(12) NWAP_CASE(13) NWAP_CASE(14) NWAP_CASE(15) NWAP_CASE(16)  \
+    NWAP_CASE(17) NWAP_CASE(18) NWAP_CASE(19) NWAP_CASE(20) NWAP_CASE(21) NWAP_CASE(22) NWAP_CASE(23) NWAP_CASE(24) \
+    NWAP_CASE(25) NWAP_CASE(26) NWAP_CASE(27) NWAP_CASE(28) NWAP_CASE(29) NWAP_CASE(30) NWAP_CASE(31) NWAP_CASE(32)
 
 // One chunk (64 sorted columns, 2 per lane) against every staged row of the band.
 // mixmode: 0 = every lane of the warp has both words of length LB; 1 = some are LB-1 (the
@@ -151,18 +238,15 @@ __device__ __forceinline__ void nwap_row_dp(const nwap_sym2 *sym, int la, const 
 template <int FLAVOR, int QMAX, int QW>
 __device__ __forceinline__ void nwap_run_chunk(int LB, nwap_tile_smem &sm, const nwap_scheme_consts &sc,
                                                const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
-                                               int l0, int l1, uint32_t off0, uint32_t off1,
-                                               int mixmode, bool fast, int want_hist, nwap_lane_stats &ls)
+                                               const nwap_lane_cols &c, int mixmode, bool fast,
+                                               int want_hist, nwap_lane_stats &ls)
 {
     uint32_t nb[QMAX];
 #pragma unroll
     for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
-    // column potentials, packed; the BIAS stays in (halves of t are score + BIAS)
-    const uint32_t kpos2 = (uint32_t)(sc.beta * l0) + ((uint32_t)(sc.beta * l1) << 16);
-    // per-lane masks selecting v (length LB) or vm1 (length LB-1) for each half
-    const uint32_t keep_v = (l0 == LB ? 0xffffu : 0u) | (l1 == LB ? 0xffff0000u : 0u);
-    uint32_t acc = 0, acc_hi = 0;     // per-chunk packed sums of t (<= 16 rows: no overflow)
-    int rows_fast = 0;
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+    const bool deep = mixmode > 1;
+    const int l0 = c.l0, l1 = c.l1;
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
         const nwap_row_meta &m = sm.meta[rr];
@@ -170,64 +254,69 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, nwap_tile_smem &sm, const
         if (la == 0) continue;                       // uniform across the CTA
         const nwap_sym2 *sym = sm.rowsym[rr];
         uint32_t v = 0, vm1 = 0;
-#if NWAP_COLD_FAMILY
-        if (mixmode < 2) {
-            NWAP_DP_SWITCH(nwap_false())
-            if (mixmode) v = (v & keep_v) | (vm1 & ~keep_v);
-        } else {
-            NWAP_DP_SWITCH(nwap_true())
-        }
-#else
-        const bool deep = mixmode > 1;               // full select inlined in every length body
-        NWAP_DP_SWITCH(deep)
-        if (mixmode == 1) v = (v & keep_v) | (vm1 & ~keep_v);
-#endif
-        const uint32_t t = v + m.ala2 + kpos2;       // halves: score + BIAS (never negative)
-        const uint32_t thi = t >> 16;
-        const int adj = m.rowadj;
-        if (fast) {
-            sm.out[adj + (int)off0] = (uint8_t)t;
-            sm.out[adj + (int)off1] = (uint8_t)thi;
-            ls.mn2 = __vmins2(ls.mn2, t);
-            ls.mx2 = __vmaxs2(ls.mx2, t);
-            acc += t;
-            acc_hi += thi;
-            ++rows_fast;
-        } else {
-            const uint32_t clo = (uint32_t)m.clo_off;
-            const uint32_t seg = (uint32_t)m.seglen;
-            const int s0 = (int)(t & 0xffffu) - (int)NWAP_BIAS;
-            const int s1 = (int)thi - (int)NWAP_BIAS;
-            if (off0 - clo < seg) {
-                sm.out[adj + (int)off0] = (uint8_t)(int8_t)s0;
-                ls.sum += s0; ls.count += 1;
-                ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffff0000u) | (t & 0xffffu));
-                ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffff0000u) | (t & 0xffffu));
-                if (want_hist) atomicAdd(&sm.hist[(s0 + 128) & 255], 1u);
-            }
-            if (off1 - clo < seg) {
-                sm.out[adj + (int)off1] = (uint8_t)(int8_t)s1;
-                ls.sum += s1; ls.count += 1;
-                ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffffu) | (t & 0xffff0000u));
-                ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffffu) | (t & 0xffff0000u));
-                if (want_hist) atomicAdd(&sm.hist[(s1 + 128) & 255], 1u);
-            }
-        }
-    }
-    if (rows_fast) {
-        // acc = sum(lo) + 65536 * sum(hi) (mod 2^32), acc_hi = sum(hi): both sums < 2^18
-        const uint32_t sum_lo = acc - (acc_hi << 16);
-        ls.sum += (long long)sum_lo + (long long)acc_hi - 2ll * rows_fast * (long long)NWAP_BIAS;
-        ls.count += 2 * rows_fast;
-    }
-}
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, la, nb, l0, l1, sc, v, vm1, deep);    \
+        break;
+        switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
-#undef NWAP_DP_SWITCH
+        if (mixmode == 1) v = (v & c.keep_v) | (vm1 & ~c.keep_v);
+        nwap_emit(sm, m, v, c, fast, want_hist, ls, ca);
+    }
+    nwap_close_chunk(ls, ca);
+}
+
+// Dual-chain chunk: 128 sorted columns (4 per lane), every word no longer than NWAP_DUAL_MAX.
+// A/B-tested and REJECTED (profiles/r01d_ab_dual.txt: 8.8 vs 10.5 TCUPS at DUAL_MAX=12): inside
+// the DP loops the kernel is already DPX-pipe-bound, so halving the loop overhead buys nothing
+// and the larger bodies cost instruction-cache hits.  Kept compiled out (0) for the record.
+#ifndef NWAP_DUAL_MAX
+#define NWAP_DUAL_MAX 0
+#endif
+template <int FLAVOR, int QW>
+__device__ __forceinline__ void nwap_run_chunk2(int LB, nwap_tile_smem &sm, const nwap_scheme_consts &sc,
+                                                const uint32_t (&wa0)[QW], const uint32_t (&wa1)[QW],
+                                                const uint32_t (&wb0)[QW], const uint32_t (&wb1)[QW],
+                                                const nwap_lane_cols &cA, const nwap_lane_cols &cB,
+                                                int mixmode, bool fast, int want_hist, nwap_lane_stats &ls)
+{
+    constexpr int DQ = NWAP_DUAL_MAX > 0 ? NWAP_DUAL_MAX : 1;
+    uint32_t nbA[DQ], nbB[DQ];
+#pragma unroll
+    for (int j = 0; j < DQ; ++j) {
+        nbA[j] = nwap_pack_negb(nwap_byte_of(wa0, j), nwap_byte_of(wa1, j));
+        nbB[j] = nwap_pack_negb(nwap_byte_of(wb0, j), nwap_byte_of(wb1, j));
+    }
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+    const bool deep = mixmode > 1;
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;
+        const nwap_sym2 *sym = sm.rowsym[rr];
+        uint32_t vA = 0, vAm1 = 0, vB = 0, vBm1 = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= DQ) nwap_row_dp2<(n <= DQ ? n : 1), FLAVOR>(sym, la, nbA, nbB, cA, cB, sc, vA, vAm1, vB, vBm1, deep); \
+        break;
+        switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+        if (mixmode == 1) {
+            vA = (vA & cA.keep_v) | (vAm1 & ~cA.keep_v);
+            vB = (vB & cB.keep_v) | (vBm1 & ~cB.keep_v);
+        }
+        nwap_emit(sm, m, vA, cA, fast, want_hist, ls, ca);
+        nwap_emit(sm, m, vB, cB, fast, want_hist, ls, ca);
+    }
+    // two emits per row: rows_fast counted twice, which is what nwap_close_chunk expects (2 scores each)
+    nwap_close_chunk(ls, ca);
+}
 
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
 // accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
 template <int FLAVOR, int QMAX>
-__global__ void __launch_bounds__(NWAP_THREADS, (QMAX <= 24 ? 5 : 4))
+__global__ void __launch_bounds__(NWAP_THREADS, (QMAX <= 24 ? NWAP_MINB : (NWAP_MINB > 4 ? 4 : NWAP_MINB)))
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -287,10 +376,13 @@ k_score_tiles(const nwap_tile_params p)
         }
         __syncthreads();
         if (tid == 0) {
-            int run = 0;
-            for (int len = MAXL; len >= 1; --len)
+            int run = 0, nlong = 0;
+            for (int len = MAXL; len >= 1; --len) {
                 for (int w = 0; w < NWAP_WARPS; ++w) { int cnt = sm.bins[w][len]; sm.bins[w][len] = run; run += cnt; }
+                if (len == NWAP_DUAL_MAX + 1) nlong = run;      // columns with words longer than NWAP_DUAL_MAX
+            }
             sm.ncols = run;
+            sm.n_long_chunks = NWAP_DUAL_MAX > 0 ? (nlong + NWAP_CHUNK - 1) / NWAP_CHUNK : (run + NWAP_CHUNK - 1) / NWAP_CHUNK;
         }
         __syncthreads();
 #pragma unroll
@@ -330,11 +422,11 @@ k_score_tiles(const nwap_tile_params p)
                 }
                 sm.meta[tid] = m;
             }
-            // stage row symbols, packed a*65537 (4 symbols per thread, R*MAXL/4 <= 128 threads)
-            {
-                const int rr = tid / (NWAP_MAXLEN_FAST / 4), q4 = tid % (NWAP_MAXLEN_FAST / 4);
+            // stage row symbols, packed a*65537, with the row boundary values (4 symbols per item)
+            for (int item = tid; item < NWAP_R * (NWAP_MAXLEN_FAST / 4); item += NWAP_THREADS) {
+                const int rr = item / (NWAP_MAXLEN_FAST / 4), q4 = item % (NWAP_MAXLEN_FAST / 4);
                 const int64_t r = rb0 + rr;
-                if (rr < NWAP_R && q4 < QW && r >= rmin && r <= rmax) {
+                if (q4 < QW && r >= rmin && r <= rmax) {
                     const uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(p.ids + r * p.qpad) + q4);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -360,22 +452,21 @@ k_score_tiles(const nwap_tile_params p)
             // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
             const int ncols = sm.ncols;
             const bool band_simple = sm.band_simple != 0;
+            const int nlc = sm.n_long_chunks;
             for (;;) {
-                int ch = 0;
-                if (lane == 0) ch = atomicAdd(&sm.next_chunk, 1);
-                ch = __shfl_sync(0xffffffffu, ch, 0);
-                const int kc = ch * NWAP_CHUNK;
+                int item = 0;
+                if (lane == 0) item = atomicAdd(&sm.next_chunk, 1);
+                item = __shfl_sync(0xffffffffu, item, 0);
+                // items 0..nlc-1: single 64-column chunks (long words); then 128-column dual chunks
+                const int kc = item < nlc ? item * NWAP_CHUNK : nlc * NWAP_CHUNK + (item - nlc) * 2 * NWAP_CHUNK;
                 if (kc >= ncols) break;
+                const bool dual = item >= nlc && (ncols - kc) > NWAP_CHUNK;
                 const int LB = sm.clen[kc];
                 const int ka = kc + 2 * lane, kb = ka + 1;
                 const bool va = ka < ncols, vb = kb < ncols;
                 const int la_ = va ? (int)sm.clen[ka] : LB, lb_ = vb ? (int)sm.clen[kb] : LB;
                 const uint32_t off0 = va ? (uint32_t)sm.cols[ka] : 0xffffu;
                 const uint32_t off1 = vb ? (uint32_t)sm.cols[kb] : 0xffffu;
-                const int lmin = min(la_, lb_);
-                const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
-                                  : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
-                const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
                 // column words (invalid lanes re-read the chunk's first column; their results are dropped)
                 const int64_t ca = strip_lo + (va ? sm.cols[ka] : sm.cols[kc]);
                 const int64_t cb = strip_lo + (vb ? sm.cols[kb] : sm.cols[kc]);
@@ -387,8 +478,37 @@ k_score_tiles(const nwap_tile_params p)
                     w0[4 * v] = x.x; w0[4 * v + 1] = x.y; w0[4 * v + 2] = x.z; w0[4 * v + 3] = x.w;
                     w1[4 * v] = y.x; w1[4 * v + 1] = y.y; w1[4 * v + 2] = y.z; w1[4 * v + 3] = y.w;
                 }
-                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, la_, lb_, off0, off1, mixmode, fast,
-                                                 p.want_hist, ls);
+                const nwap_lane_cols cA = nwap_make_lane_cols(off0, off1, la_, lb_, LB, sc);
+                if (!dual) {
+                    const int lmin = min(la_, lb_);
+                    const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
+                                      : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
+                    const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
+                    nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+                } else {
+                    const int kc2 = kc + NWAP_CHUNK;
+                    const int kd = kc2 + 2 * lane, ke = kd + 1;
+                    const bool vd = kd < ncols, ve = ke < ncols;
+                    const int ld_ = vd ? (int)sm.clen[kd] : LB, le_ = ve ? (int)sm.clen[ke] : LB;
+                    const uint32_t off2 = vd ? (uint32_t)sm.cols[kd] : 0xffffu;
+                    const uint32_t off3 = ve ? (uint32_t)sm.cols[ke] : 0xffffu;
+                    const int64_t cd = strip_lo + (vd ? sm.cols[kd] : sm.cols[kc]);
+                    const int64_t ce = strip_lo + (ve ? sm.cols[ke] : sm.cols[kc]);
+                    uint32_t w2[QW], w3[QW];
+#pragma unroll
+                    for (int v = 0; v < QW / 4; ++v) {
+                        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p.ids + cd * p.qpad) + v);
+                        const uint4 y = __ldg(reinterpret_cast<const uint4 *>(p.ids + ce * p.qpad) + v);
+                        w2[4 * v] = x.x; w2[4 * v + 1] = x.y; w2[4 * v + 2] = x.z; w2[4 * v + 3] = x.w;
+                        w3[4 * v] = y.x; w3[4 * v + 1] = y.y; w3[4 * v + 2] = y.z; w3[4 * v + 3] = y.w;
+                    }
+                    const nwap_lane_cols cB = nwap_make_lane_cols(off2, off3, ld_, le_, LB, sc);
+                    const int lmin = min(min(la_, lb_), min(ld_, le_));
+                    const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
+                                      : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
+                    const bool fast = band_simple && (kc + 2 * NWAP_CHUNK <= ncols);
+                    nwap_run_chunk2<FLAVOR, QW>(LB, sm, sc, w0, w1, w2, w3, cA, cB, mixmode, fast, p.want_hist, ls);
+                }
             }
             __syncthreads();
 
