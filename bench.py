@@ -160,6 +160,16 @@ def cpu_reference_run(ids, lens, scheme, budget_s: float, threads: int):
     return {"pairs": pairs, "cells": cells, "seconds": dt, "chunks": len(starts)}
 
 
+def traffic_from_profile(n_words: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_score_tiles launch from the committed
+    `ncu --set full` capture of this workload (profiles/traffic.json), or None."""
+    f = ROOT / "profiles" / "traffic.json"
+    if not f.exists():
+        return None
+    rec = json.loads(f.read_text()).get(str(n_words))
+    return rec["dram_bytes_per_launch"] if rec else None
+
+
 def numpy_port_rate(ids, lens, scheme, chunks: int = 2):
     """Single-process rate of the numpy restatement of the reference's batched engine."""
     from oracle import nw_oracle as orc
@@ -297,7 +307,9 @@ def main():
     roof = None
     if rank == 0:
         kern_ms = float(np.mean(step_ms))                 # one k_score_tiles launch per step (+1 tiny init)
-        ipc_mix, _ = probe("mix_2alu_2imad", 4000, local_rank)
+        # the packed cell's exact instruction mix (2 DPX + 1 IMAD + 1 IADD for the default variant)
+        mix_name = "mix_2alu_2imad" if args.variant == "packed" else "cell_2dpx_imad_iadd"
+        ipc_mix, _ = probe(mix_name, 4000, local_rank)
         ipc_alu, _ = probe("vimnmx3_s16x2", 4000, local_rank)
         ipc_imad, _ = probe("imad", 4000, local_rank)
         sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
@@ -310,11 +322,12 @@ def main():
         roof = {
             "bound": "int-alu (DPX/IMAD issue; SURVEY 8(d): not hbm, not tensor)",
             "achieved": achieved, "peak": peak_gcups, "unit": "GCUPS", "frac": achieved / peak_gcups,
-            "traffic": None,
+            "traffic": traffic_from_profile(n),
             "kernel": "k_score_tiles", "kernel_ms": kern_ms,
-            "peak_how": (f"live probe: {ipc_mix:.3f} warp-instr/clk/SM on the packed cell's 2 ALU + 2 IMAD mix "
-                         f"x 16 cells/instr x {SM_COUNT} SMs x {sm_max:.0f} MHz (clocks.max.sm); "
-                         f"single-pipe probes: VIMNMX3.S16x2 {ipc_alu:.3f}, IMAD {ipc_imad:.3f}"),
+            "algorithmic_bytes": int(shard_pairs),
+            "peak_how": (f"live probe {mix_name}: {ipc_mix:.3f} warp-instr/clk/SM on the packed cell's own 4-instruction "
+                         f"mix x 16 cells/instr x {SM_COUNT} SMs x {sm_max:.0f} MHz (clocks.max.sm); "
+                         f"single-pipe probes: VIMNMX3.S16x2 {ipc_alu:.3f}, IMAD {ipc_imad:.3f} (both half-rate)"),
             "sm_mhz_under_load": sm_now,
             "frac_at_observed_clock": achieved / (16.0 * ipc_mix * SM_COUNT * sm_now * 1e6 / 1e9),
             "hbm_write": {"achieved": shard_pairs / (kern_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
