@@ -305,6 +305,52 @@ def test_c3_two_independent_kernels_agree():
         assert tuple(tot) == sa[:4] and np.array_equal(hist, sa[4])
 
 
+def _slab_pass(ctx, variant, slab_bytes, want_hist=True, lo=0, hi=None):
+    """Score [lo, hi) slab by slab into one reused device buffer; returns merged statistics."""
+    hi = ctx.num_edges if hi is None else hi
+    buf = torch.empty(slab_bytes, dtype=torch.int8, device="cuda")
+    tot = [0, 127, -128, 0]
+    hist = np.zeros(256, dtype=np.int64)
+    for s in range(lo, hi, slab_bytes):
+        e = min(hi, s + slab_bytes)
+        st = ctx.score_range(s, e, buf, want_hist=want_hist, variant=variant)
+        tot = [tot[0] + st[0], min(tot[1], st[1]), max(tot[2], st[2]), tot[3] + st[3]]
+        if want_hist:
+            hist += st[4]
+    return tuple(tot), hist
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_full_scale_600k_two_kernels_agree(cfg, golden_samples):
+    """configs[3]/[4] at FULL size on one GPU (179,999,700,000 pairs, scored slab by slab):
+    the packed DPX kernel's 256-bin histogram, int64 sum, min, max and count must equal those of
+    the independent one-thread-per-pair kernel on a fixed 1/16 sample of slabs, and its whole-job
+    count must be exact (SURVEY 8(d) bit-exactness protocol for C4/C5)."""
+    meta, _ = golden_samples
+    ids, lens, sch = synth.config_store(cfg)
+    with NwapContext(ids, lens, nw.ScoringScheme(*sch)) as ctx:
+        P = ctx.num_edges
+        assert P == 179_999_700_000
+        slab = 2_000_000_000
+        tot, hist = _slab_pass(ctx, "packed", slab)
+        assert tot[3] == P == int(hist.sum())
+        assert int((hist * (np.arange(256) - 128)).sum()) == tot[0]
+        nz = np.flatnonzero(hist)
+        assert (int(nz[0]) - 128, int(nz[-1]) - 128) == (tot[1], tot[2])
+        # both packed flavours agree on the whole job
+        tot0, hist0 = _slab_pass(ctx, "packed3", slab)
+        assert tot0 == tot and np.array_equal(hist0, hist)
+        # independent kernel on every 16th 500 M-edge window (11.25e9 pairs)
+        win = 500_000_000
+        for k, s in enumerate(range(0, P, win)):
+            if k % 16 != 3:
+                continue
+            e = min(P, s + win)
+            a, ha = _slab_pass(ctx, "packed", win, lo=s, hi=e)
+            b, hb = _slab_pass(ctx, "simple", win, lo=s, hi=e)
+            assert a == b and np.array_equal(ha, hb), (cfg, s)
+
+
 # ---- new surface: compaction, degree, index recovery ----------------------------------------
 
 def test_compaction_and_degree(golden_cases):
