@@ -129,6 +129,22 @@ int nwap_compact_range(nwap_ctx *ctx, const int8_t *payload_dev, int64_t start, 
                        int threshold, int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap,
                        int64_t *count_host, int32_t *degree_dev, void *stream);
 
+/* graph.py:91-101 filter_view keep-mask on the device: keep the edges of an already scored
+ * slice whose NORMALISED weight w = 100.0 * score / max(len_r, len_c) satisfies
+ * lo <= w <= hi, evaluated in IEEE double exactly as numpy does (graph.py:96-98).
+ * Outputs and degree as for nwap_compact_range; lo > hi is NWAP_EINVAL (graph.py:86-87). */
+int nwap_filter_normalized(nwap_ctx *ctx, const int8_t *payload_dev, int64_t start, int64_t end,
+                           double lo, double hi, int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap,
+                           int64_t *count_host, int32_t *degree_dev, void *stream);
+
+/* store.py:342-381 histogram(normalized=True): counts_dev[v + 12800] += 1 for
+ * v = floor(100*score / max(len_r, len_c)) (exact integer floor division, store.py:360);
+ * counts_dev is a (25501,) uint64 device array, NOT zeroed here.  Asynchronous on `stream`. */
+#define NWAP_NHIST_BINS 25501
+#define NWAP_NHIST_FIRST (-12800)
+int nwap_hist_normalized(nwap_ctx *ctx, const int8_t *payload_dev, int64_t start, int64_t end,
+                         uint64_t *counts_dev, void *stream);
+
 /* split [0, num_edges) into `parts` contiguous ranges of equal DP
  * cells.  bounds_out has parts+1 entries, bounds_out[0]=0, bounds_out[parts]=P.
  * Host-side arithmetic only. */

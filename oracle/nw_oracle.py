@@ -289,6 +289,31 @@ def np_compact(payload: np.ndarray, start: int, n: int, threshold: int):
     return idx, payload[keep], degree.astype(np.int64)
 
 
+def np_filter_normalized(payload: np.ndarray, start: int, n: int, lengths, lo: float, hi: float):
+    """graph.py:91-101 restated: keep edges with lo <= 100.0*score/max(len_r,len_c) <= hi in float64.
+    Returns (idx int64, score int8, degree int64[n])."""
+    payload = np.asarray(payload, dtype=np.int8)
+    L = np.asarray(lengths, dtype=np.int64)
+    idx_all = np.arange(start, start + payload.size, dtype=np.int64)
+    rows = np_rows_of(idx_all, n)
+    cols = np_cols_of(idx_all, n, rows)
+    w = (100.0 * payload) / np.maximum(L[rows], L[cols])
+    keep = (w >= lo) & (w <= hi)
+    degree = np.bincount(rows[keep], minlength=n) + np.bincount(cols[keep], minlength=n)
+    return idx_all[keep], payload[keep], degree.astype(np.int64)
+
+
+def np_hist_normalized(payload: np.ndarray, start: int, n: int, lengths) -> np.ndarray:
+    """store.py:352-366 (normalized=True): 25501 bins, bin b counts floor(100*s/max_len) == b-12800."""
+    payload = np.asarray(payload, dtype=np.int8)
+    L = np.asarray(lengths, dtype=np.int64)
+    idx_all = np.arange(start, start + payload.size, dtype=np.int64)
+    rows = np_rows_of(idx_all, n)
+    cols = np_cols_of(idx_all, n, rows)
+    values = np.floor_divide(100 * payload.astype(np.int64), np.maximum(L[rows], L[cols]))
+    return np.bincount(values + 12800, minlength=25501).astype(np.int64)
+
+
 def np_histogram(payload: np.ndarray) -> np.ndarray:
     """store.py:352-366 (raw mode): 256 bins, bin k counts score k-128."""
     return np.bincount(np.asarray(payload, dtype=np.int8).astype(np.int64) + 128,

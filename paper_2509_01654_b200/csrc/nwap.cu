@@ -433,9 +433,9 @@ int nwap_payload_stats(nwap_ctx *c, const int8_t *payload_dev, int64_t count, nw
     return fetch_stats(c, stats_host, st);
 }
 
-int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end, int threshold,
-                       int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
-                       int32_t *degree_dev, void *stream)
+static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end, int mode,
+                          const nwap_keep_params &kp, int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap,
+                          int64_t *count_host, int32_t *degree_dev, cudaStream_t st)
 {
     if (!c || !count_host) return fail(NWAP_EINVAL, "null argument");
     const int64_t P = nwap_num_edges(c);
@@ -446,7 +446,6 @@ int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, in
     if (count == 0) return NWAP_OK;
     if (!payload_dev) return fail(NWAP_EINVAL, "null payload");
     CK(cudaSetDevice(c->device));
-    cudaStream_t st = (cudaStream_t)stream;
     const int64_t nblocks = (count + NWAP_CMP_BLOCK - 1) / NWAP_CMP_BLOCK;
     if (nblocks > 0x7fffffffLL) return fail(NWAP_EINVAL, "range too large for one compaction call; split it");
     if (c->block_counts_cap < nblocks) {
@@ -454,11 +453,11 @@ int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, in
         CK(cudaMalloc(&c->d_block_counts, sizeof(long long) * (size_t)nblocks));
         c->block_counts_cap = nblocks;
     }
-    k_compact_count<<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, threshold, c->d_block_counts);
+    if (mode == 0) k_compact_count<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts);
+    else k_compact_count<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts);
     k_compact_scan<<<1, 1024, 0, st>>>(c->d_block_counts, nblocks, c->d_total);
-    k_compact_write<<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, start, c->n, threshold,
-                                                                  c->d_block_counts, idx_out_dev, score_out_dev, cap,
-                                                                  degree_dev);
+    if (mode == 0) k_compact_write<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, idx_out_dev, score_out_dev, cap, degree_dev);
+    else k_compact_write<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, idx_out_dev, score_out_dev, cap, degree_dev);
     g_launches += 3;
     CK(cudaGetLastError());
     long long total = 0;
@@ -466,6 +465,52 @@ int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, in
     CK(cudaStreamSynchronize(st));
     *count_host = total;
     if (total > cap) return fail(NWAP_ECAPACITY, "compaction kept %lld edges but capacity is %lld", total, (long long)cap);
+    return NWAP_OK;
+}
+
+int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end, int threshold,
+                       int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
+                       int32_t *degree_dev, void *stream)
+{
+    if (!c) return fail(NWAP_EINVAL, "null context");
+    nwap_keep_params kp;
+    kp.threshold = threshold; kp.lo = 0; kp.hi = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    return compact_common(c, payload_dev, start, end, 0, kp, idx_out_dev, score_out_dev, cap, count_host, degree_dev,
+                          (cudaStream_t)stream);
+}
+
+int nwap_filter_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end, double lo, double hi,
+                           int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
+                           int32_t *degree_dev, void *stream)
+{
+    if (!c) return fail(NWAP_EINVAL, "null context");
+    if (lo > hi) return fail(NWAP_EINVAL, "empty filter range: lo=%g > hi=%g", lo, hi);
+    nwap_keep_params kp;
+    kp.threshold = 0; kp.lo = lo; kp.hi = hi; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    return compact_common(c, payload_dev, start, end, 1, kp, idx_out_dev, score_out_dev, cap, count_host, degree_dev,
+                          (cudaStream_t)stream);
+}
+
+int nwap_hist_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end,
+                         uint64_t *counts_dev, void *stream)
+{
+    if (!c || !counts_dev) return fail(NWAP_EINVAL, "null argument");
+    const int64_t P = nwap_num_edges(c);
+    if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
+    const int64_t count = end - start;
+    if (count == 0) return NWAP_OK;
+    if (!payload_dev) return fail(NWAP_EINVAL, "null payload");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    nwap_keep_params kp;
+    kp.threshold = 0; kp.lo = 0; kp.hi = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    const size_t smem = sizeof(unsigned int) * NWAP_NHIST_SPAN;
+    CK(cudaFuncSetAttribute(k_hist_normalized, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t runs = (count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((runs + 511) / 512, (int64_t)c->sm_count * 2));
+    k_hist_normalized<<<(unsigned)blocks, 512, smem, st>>>(payload_dev, count, kp, (unsigned long long *)counts_dev);
+    g_launches++;
+    CK(cudaGetLastError());
     return NWAP_OK;
 }
 

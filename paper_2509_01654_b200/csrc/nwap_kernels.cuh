@@ -706,20 +706,69 @@ k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stat
 }
 
 // ---------------------------------------------------------------------------
-// Ordered threshold compaction: count per block -> exclusive scan -> write.
+// Ordered compaction: count per block -> exclusive scan -> write.  The keep predicate is
+//   MODE 0: raw score >= threshold
+//   MODE 1: lo <= 100.0 * score / max(len_r, len_c) <= hi in IEEE double, exactly the
+//           keep-mask of reference graph.py:96-98 (numpy float64 true division)
+// Each thread owns 16 consecutive edges; for MODE 1 it recovers (r, c) of its first edge
+// once (fp64 estimate + integer fix-up) and then walks the triangle.
 // ---------------------------------------------------------------------------
 #define NWAP_CMP_THREADS 256
 #define NWAP_CMP_PER_THREAD 16
 #define NWAP_CMP_BLOCK (NWAP_CMP_THREADS * NWAP_CMP_PER_THREAD)   // 4096 edges per block
 
+struct nwap_keep_params {
+    int threshold;           // MODE 0
+    double lo, hi;           // MODE 1
+    const uint8_t *lens;     // MODE 1
+    int64_t n;
+    int64_t start;           // linear index of payload[0]
+};
+
+// keep-bits (bit k = edge base+k kept) of one thread's run of 16 edges
+template <int MODE>
+__device__ __forceinline__ unsigned nwap_keep_bits(const int8_t *__restrict__ payload, int64_t count, int64_t base,
+                                                   const nwap_keep_params &kp, int8_t (&v)[NWAP_CMP_PER_THREAD])
+{
+    unsigned bits = 0;
+    if (base >= count) {
+#pragma unroll
+        for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) v[k] = 0;
+        return 0;
+    }
+    int64_t r = 0, c = 0;
+    if (MODE == 1) {
+        r = nwap_row_of(kp.start + base, kp.n);
+        c = nwap_col_of(kp.start + base, kp.n, r);
+    }
+#pragma unroll
+    for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) {
+        const bool in = base + k < count;
+        v[k] = in ? payload[base + k] : (int8_t)0;
+        bool keep;
+        if (MODE == 0) {
+            keep = in && (int)v[k] >= kp.threshold;
+        } else {
+            keep = false;
+            if (in) {
+                const int m = max((int)kp.lens[r], (int)kp.lens[c]);
+                const double w = (100.0 * (double)v[k]) / (double)m;
+                keep = (w >= kp.lo) && (w <= kp.hi);
+                if (++c == kp.n) { ++r; c = r + 1; }
+            }
+        }
+        bits |= (keep ? 1u : 0u) << k;
+    }
+    return bits;
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(NWAP_CMP_THREADS)
-k_compact_count(const int8_t *__restrict__ payload, int64_t count, int threshold, long long *block_counts)
+k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, long long *block_counts)
 {
     const int64_t base = (int64_t)blockIdx.x * NWAP_CMP_BLOCK + (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD;
-    int kept = 0;
-#pragma unroll
-    for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k)
-        if (base + k < count && (int)payload[base + k] >= threshold) ++kept;
+    int8_t v[NWAP_CMP_PER_THREAD];
+    int kept = __popc(nwap_keep_bits<MODE>(payload, count, base, kp, v));
     __shared__ int wsum[NWAP_CMP_THREADS / 32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
@@ -770,19 +819,15 @@ k_compact_scan(long long *block_counts, int64_t nblocks, long long *total_out)
     if (threadIdx.x == 0) *total_out = carry;
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(NWAP_CMP_THREADS)
-k_compact_write(const int8_t *__restrict__ payload, int64_t count, int64_t start, int64_t n, int threshold,
-                const long long *block_offsets, int64_t *idx_out, int8_t *score_out, int64_t cap,
-                int *degree)
+k_compact_write(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp,
+                const long long *block_offsets, int64_t *idx_out, int8_t *score_out, int64_t cap, int *degree)
 {
     const int64_t base = (int64_t)blockIdx.x * NWAP_CMP_BLOCK + (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD;
     int8_t v[NWAP_CMP_PER_THREAD];
-    int kept = 0;
-#pragma unroll
-    for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) {
-        v[k] = (base + k < count) ? payload[base + k] : (int8_t)-128;
-        if (base + k < count && (int)v[k] >= threshold) ++kept;
-    }
+    const unsigned bits = nwap_keep_bits<MODE>(payload, count, base, kp, v);
+    const int kept = __popc(bits);
     // exclusive scan of `kept` over the block
     __shared__ int wtot[NWAP_CMP_THREADS / 32];
     int x = kept;
@@ -796,20 +841,60 @@ k_compact_write(const int8_t *__restrict__ payload, int64_t count, int64_t start
     int woff = 0;
     for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) woff += wtot[w];
     int64_t pos = block_offsets[blockIdx.x] + woff + (x - kept);
+    if (!bits) return;
 #pragma unroll
     for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) {
-        if (base + k < count && (int)v[k] >= threshold) {
-            const int64_t idx = start + base + k;
+        if ((bits >> k) & 1u) {
+            const int64_t idx = kp.start + base + k;
             if (pos < cap) { idx_out[pos] = idx; score_out[pos] = v[k]; }
             if (degree) {
-                const int64_t r = nwap_row_of(idx, n);
-                const int64_t c = nwap_col_of(idx, n, r);
+                const int64_t r = nwap_row_of(idx, kp.n);
+                const int64_t c = nwap_col_of(idx, kp.n, r);
                 atomicAdd(&degree[r], 1);
                 atomicAdd(&degree[c], 1);
             }
             ++pos;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Normalised histogram (reference store.py:352-366, normalized=True): bin of
+// floor(100*score / max(len_r, len_c)) in exact integer arithmetic, values in
+// [-12800, 12700] -> 25,501 bins.  Counts are privatised per CTA in shared memory
+// (25,501 x u32 = 100 KB) and flushed once.
+// ---------------------------------------------------------------------------
+#define NWAP_NHIST_OFFSET (-12800)
+#define NWAP_NHIST_SPAN 25501
+
+__global__ void __launch_bounds__(512)
+k_hist_normalized(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp,
+                  unsigned long long *counts)
+{
+    extern __shared__ unsigned int sbins[];
+    for (int b = threadIdx.x; b < NWAP_NHIST_SPAN; b += blockDim.x) sbins[b] = 0;
+    __syncthreads();
+    // each CTA takes a contiguous slice; each thread walks runs of 16 edges
+    const int64_t runs = (count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
+    for (int64_t run = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; run < runs; run += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t base = run * NWAP_CMP_PER_THREAD;
+        int64_t r = nwap_row_of(kp.start + base, kp.n);
+        int64_t c = nwap_col_of(kp.start + base, kp.n, r);
+#pragma unroll
+        for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) {
+            if (base + k < count) {
+                const int m = max((int)kp.lens[r], (int)kp.lens[c]);
+                const int num = 100 * (int)payload[base + k];
+                int q = num / m;
+                if ((num % m != 0) && (num < 0)) --q;           // floor division
+                atomicAdd(&sbins[q - NWAP_NHIST_OFFSET], 1u);
+                if (++c == kp.n) { ++r; c = r + 1; }
+            }
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NWAP_NHIST_SPAN; b += blockDim.x)
+        if (sbins[b]) atomicAdd(&counts[b], (unsigned long long)sbins[b]);
 }
 
 __global__ void k_rows_cols(int64_t n, const int64_t *idx, int64_t count, int64_t *rows, int64_t *cols)

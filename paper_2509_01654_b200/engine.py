@@ -214,6 +214,42 @@ class NwapContext:
         return idx[: cnt.value], sc[: cnt.value]
 
 
+    def filter_normalized(self, payload, start: int, end: int, lo: float, hi: float, capacity: int,
+                          degree=None):
+        """Reference graph.py:91-101 keep-mask on the device: edges of an already scored slice with
+        lo <= 100*score/max(len_r, len_c) <= hi (float64, as numpy).  Returns (idx, score) tensors in
+        index order; ``degree`` gets +1 at both endpoints of every kept edge."""
+        import torch
+
+        if lo > hi:
+            raise ValueError(f"empty filter range: lo={lo} > hi={hi}")
+        dev = payload.device
+        idx = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
+        sc = torch.empty(max(capacity, 1), dtype=torch.int8, device=dev)
+        cnt = ctypes.c_int64()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = lib().nwap_filter_normalized(self._h, payload.data_ptr(), start, end, float(lo), float(hi),
+                                          idx.data_ptr(), sc.data_ptr(), capacity, ctypes.addressof(cnt),
+                                          degree.data_ptr() if degree is not None else None, stream)
+        if rc == _native.NWAP_ECAPACITY:
+            raise _native.CapacityError(_native.last_error(), cnt.value)
+        check(rc)
+        return idx[: cnt.value], sc[: cnt.value]
+
+    def hist_normalized(self, payload, start: int, end: int, counts=None):
+        """Reference store.py:342-381 histogram(normalized=True) on the device: returns a (25501,)
+        int64 CUDA tensor, bin b counting floor(100*score/max(len_r,len_c)) == b - 12800.  Pass
+        ``counts`` to accumulate over several slices."""
+        import torch
+
+        dev = payload.device
+        if counts is None:
+            counts = torch.zeros(25501, dtype=torch.int64, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        check(lib().nwap_hist_normalized(self._h, payload.data_ptr(), start, end, counts.data_ptr(), stream))
+        return counts
+
+
 def _host_ptr(buf):
     if isinstance(buf, np.ndarray):
         if not buf.flags["C_CONTIGUOUS"] or buf.itemsize != 1:

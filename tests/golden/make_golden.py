@@ -170,6 +170,37 @@ def main():
     np.savez_compressed(HERE / "sampled_ranges.npz", **samples)
     (HERE / "sampled_ranges.json").write_text(json.dumps({"C1": c1, **sample_meta}, indent=1))
 
+    # ---- downstream consumers of the payload, run by the reference itself --
+    import tempfile
+    from phonsim.graph import filter_view
+    from phonsim.store import EdgeStore, EdgeStoreWriter, histogram
+    words = ref_make_words(n=500, seed=500, alphabet=30, min_len=2, max_len=10)
+    scheme = ScoringScheme(1, -1, -1)
+    with tempfile.TemporaryDirectory() as tmp:
+        prefix = Path(tmp) / "g"
+        writer = EdgeStoreWriter(prefix, words, scheme)
+        compute_all_pairs(words, scheme, writer, ComputePlan(n=500, scheme=scheme))
+        writer.finalize()
+        store = EdgeStore(prefix)
+        cons = {}
+        for nm, normalized in (("raw", False), ("norm", True)):
+            h = histogram(store, words, normalized=normalized)
+            cons[f"hist_{nm}_first"] = np.array([h.min], dtype=np.int64)
+            cons[f"hist_{nm}_counts"] = np.array(h.counts, dtype=np.int64)
+        for k, (lo, hi) in enumerate([(20.0, 60.0), (-100.0, -50.5), (0.0, 0.0), (33.3, 1e9), (-1e9, 1e9)]):
+            view = filter_view(store, words, lo, hi)
+            edges = sorted((u, v) for u, adj in view.adjacency.items() for v, _ in adj if u < v)
+            cons[f"filter{k}_bounds"] = np.array([lo, hi], dtype=np.float64)
+            cons[f"filter{k}_count"] = np.array([len(edges)], dtype=np.int64)
+            if len(edges) <= 30000:          # the all-pass window is pinned by count + degree only
+                cons[f"filter{k}_edges"] = np.array(edges, dtype=np.int32).reshape(-1, 2)
+            deg = np.zeros(500, dtype=np.int64)
+            for u, adj in view.adjacency.items():
+                deg[u] = len(adj)
+            cons[f"filter{k}_degree"] = deg
+        store.close()
+    np.savez_compressed(HERE / "consumers_seed500.npz", **cons)
+
     # ---- triangle: reference rows/cols at large n ----------------------------
     tri = {}
     rng = np.random.default_rng(42)

@@ -388,6 +388,58 @@ def test_c5_threshold_compaction_slab(golden_samples):
         assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
 
 
+def test_normalized_filter_and_histogram_match_reference(golden_cases):
+    """graph.py:91-101 keep-mask and store.py:342-381 normalised histogram on
+    the device, against vectors produced by the reference's own filter_view / histogram."""
+    c = golden_cases["seed500"]
+    g = np.load(GOLDEN / "consumers_seed500.npz")
+    n, P = 500, nw.num_edges(500)
+    with NwapContext(c["ids"], c["lengths"], _scheme(c)) as ctx:
+        out = torch.empty(P, dtype=torch.int8, device="cuda")
+        ctx.score_range(0, P, out)
+        hn = ctx.hist_normalized(out, 0, P).cpu().numpy()
+        first = int(g["hist_norm_first"][0])
+        ref = np.zeros(25501, dtype=np.int64)
+        ref[first + 12800: first + 12800 + len(g["hist_norm_counts"])] = g["hist_norm_counts"]
+        assert np.array_equal(hn, ref)
+        for k in range(5):
+            lo, hi = (float(x) for x in g[f"filter{k}_bounds"])
+            degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+            idx, sc = ctx.filter_normalized(out, 0, P, lo, hi, capacity=P, degree=degree)
+            assert idx.numel() == int(g[f"filter{k}_count"][0])
+            assert np.array_equal(degree.cpu().numpy().astype(np.int64), g[f"filter{k}_degree"])
+            idx_h = idx.cpu().numpy()
+            assert np.array_equal(sc.cpu().numpy(), c["payload"][idx_h])
+            if f"filter{k}_edges" in g:
+                rows = orc.np_rows_of(idx_h, n)
+                cols = orc.np_cols_of(idx_h, n, rows)
+                assert np.array_equal(np.stack([rows, cols], 1), g[f"filter{k}_edges"].astype(np.int64))
+        # sub-range + accumulate: two halves give the same histogram; odd offsets exercise the (r, c) walk
+        acc = ctx.hist_normalized(out[: 70_001], 0, 70_001)
+        acc = ctx.hist_normalized(out[70_001:], 70_001, P, counts=acc)
+        assert np.array_equal(acc.cpu().numpy(), ref)
+        with pytest.raises(ValueError):
+            ctx.filter_normalized(out, 0, P, 2.0, 1.0, capacity=10)
+
+
+def test_normalized_consumers_on_c5_slab():
+    """The same consumers at configs[4] scale on a 3 M-edge slab, against the numpy restatement."""
+    ids, lens, sch = synth.config_store("C5")
+    n = len(lens)
+    with NwapContext(ids, lens, nw.ScoringScheme(*sch)) as ctx:
+        P = ctx.num_edges
+        s, e = 2 * (P // 3) + 17, 2 * (P // 3) + 17 + 3_000_000
+        out = torch.empty(e - s, dtype=torch.int8, device="cuda")
+        ctx.score_range(s, e, out)
+        payload = out.cpu().numpy()
+        ridx, rsc, rdeg = orc.np_filter_normalized(payload, s, n, lens, 25.0, 80.0)
+        degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+        idx, sc = ctx.filter_normalized(out, s, e, 25.0, 80.0, capacity=e - s, degree=degree)
+        assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
+        assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
+        assert np.array_equal(ctx.hist_normalized(out, s, e).cpu().numpy(), orc.np_hist_normalized(payload, s, n, lens))
+
+
 def test_device_index_recovery(golden_triangle):
     t = golden_triangle
     for n in (4, 300, 10 ** 5, 10 ** 6, 10 ** 7, 600_000):

@@ -169,3 +169,31 @@ def test_cells_and_equal_work_bounds():
             target = -((-g * W) // parts)
             assert b[g] == int(np.searchsorted(work, target, side="left"))
         assert b[0] == 0 and b[-1] == P
+
+
+# ---- downstream consumers: the reference's filter_view / histogram -------
+
+def test_consumer_oracles_match_reference(golden_cases):
+    c = golden_cases["seed500"]
+    g = np.load(GOLDEN / "consumers_seed500.npz")
+    n = 500
+    payload, lens = c["payload"], c["lengths"]
+    # raw and normalised histograms (store.py:342-381)
+    h = orc.np_histogram(payload)
+    first = int(g["hist_raw_first"][0])
+    assert np.array_equal(h[first + 128: first + 128 + len(g["hist_raw_counts"])], g["hist_raw_counts"])
+    assert h.sum() == g["hist_raw_counts"].sum()
+    hn = orc.np_hist_normalized(payload, 0, n, lens)
+    first = int(g["hist_norm_first"][0])
+    assert np.array_equal(hn[first + 12800: first + 12800 + len(g["hist_norm_counts"])], g["hist_norm_counts"])
+    assert hn.sum() == g["hist_norm_counts"].sum() == payload.size
+    # normalised filter windows (graph.py:91-101)
+    for k in range(5):
+        lo, hi = g[f"filter{k}_bounds"]
+        idx, sc, deg = orc.np_filter_normalized(payload, 0, n, lens, lo, hi)
+        assert idx.size == int(g[f"filter{k}_count"][0])
+        assert np.array_equal(deg, g[f"filter{k}_degree"])
+        if f"filter{k}_edges" in g:
+            rows = orc.np_rows_of(idx, n)
+            cols = orc.np_cols_of(idx, n, rows)
+            assert np.array_equal(np.stack([rows, cols], 1), g[f"filter{k}_edges"].astype(np.int64))
