@@ -83,7 +83,9 @@ int nwap_create(nwap_ctx **ctx_out, int device,
 
 /* ScoringScheme.overrides (aligner.py:51-65, engine.py:113-116): install a
  * dense symmetric K x K similarity table (host int8, row-major).  Symbols >= K
- * are rejected.  Routes scoring through the table-driven kernel. */
+ * are rejected.  If the table is the uniform scheme plus at most 3 overrides per symbol
+ * (and K <= 128) the packed kernel still runs it (sparse-override mode); otherwise scoring is
+ * routed through the table-driven generic kernel. */
 int nwap_set_similarity(nwap_ctx *ctx, const int8_t *sim, int K);
 
 void nwap_destroy(nwap_ctx *ctx);

@@ -41,7 +41,7 @@ int fail(int code, const char *fmt, ...)
     } while (0)
 
 static_assert(sizeof(nwap_dev_stats) == sizeof(nwap_stats), "stats layouts must agree");
-static_assert(sizeof(nwap_tile_smem) <= 227 * 1024, "tile shared memory too large");
+static_assert(sizeof(nwap_tile_smem_t<true>) <= 227 * 1024, "tile shared memory too large");
 
 }  // namespace
 
@@ -54,6 +54,8 @@ struct nwap_ctx {
     int match = 0, mismatch = 0, gap = 0;
     int K = 0;             // similarity table size (max symbol + 1 unless overridden)
     bool general = false;  // explicit similarity table installed
+    bool sparse_ov = false; // ... and it is uniform + at most NWAP_MAX_OV overrides per symbol (packed kernel can run it)
+    nwap_ov_row *d_ov = nullptr;
     std::vector<uint8_t> h_lens;        // host copy for shard arithmetic
     std::vector<int64_t> h_lenprefix;   // prefix sums of lengths (n+1)
     uint8_t *d_ids = nullptr;
@@ -70,19 +72,21 @@ struct nwap_ctx {
     int64_t slab_bytes = 0;
     cudaStream_t s_compute = nullptr, s_copy = nullptr;
     cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
-    int occ_tiles[6] = {0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor, qclass) instantiation
+    int occ_tiles[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor | ov=2, qclass) instantiation
 };
 
 namespace {
 
 typedef void (*tile_kernel_t)(const nwap_tile_params);
 
-// qclass: 0 -> rows up to 16 symbols, 1 -> up to 24, 2 -> up to 32
-tile_kernel_t tile_kernel(int flavor, int qclass)
+// qclass: 0 -> rows up to 16 symbols, 1 -> up to 24, 2 -> up to 32; ov: sparse-override build
+tile_kernel_t tile_kernel(int flavor, int qclass, bool ov)
 {
-    if (flavor == 0) return qclass == 0 ? k_score_tiles<0, 16> : qclass == 1 ? k_score_tiles<0, 24> : k_score_tiles<0, 32>;
-    return qclass == 0 ? k_score_tiles<1, 16> : qclass == 1 ? k_score_tiles<1, 24> : k_score_tiles<1, 32>;
+    if (ov) return qclass == 0 ? k_score_tiles<1, 16, true> : qclass == 1 ? k_score_tiles<1, 24, true> : k_score_tiles<1, 32, true>;
+    if (flavor == 0) return qclass == 0 ? k_score_tiles<0, 16, false> : qclass == 1 ? k_score_tiles<0, 24, false> : k_score_tiles<0, 32, false>;
+    return qclass == 0 ? k_score_tiles<1, 16, false> : qclass == 1 ? k_score_tiles<1, 24, false> : k_score_tiles<1, 32, false>;
 }
+size_t tile_smem(bool ov) { return ov ? sizeof(nwap_tile_smem_t<true>) : sizeof(nwap_tile_smem_t<false>); }
 
 int build_sim_table(nwap_ctx *c, const int8_t *sim_host)
 {
@@ -123,12 +127,12 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
                   int variant, cudaStream_t st)
 {
     if (start >= end) return NWAP_OK;
-    const bool fast_ok = !c->general && c->qmax <= NWAP_MAXLEN_FAST;
+    const bool fast_ok = (!c->general || c->sparse_ov) && c->qmax <= NWAP_MAXLEN_FAST;
     // PACKED3 (2 DPX + IMAD + IADD) measured ~8 % faster than PACKED (2 DPX + 2 IMAD): profiles/r01_ab.txt
     if (variant == NWAP_VARIANT_AUTO) variant = fast_ok ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
     if ((variant == NWAP_VARIANT_PACKED || variant == NWAP_VARIANT_PACKED3) && !fast_ok)
-        return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme and max word length <= %d (have %d%s)",
-                    NWAP_MAXLEN_FAST, c->qmax, c->general ? ", explicit similarity table" : "");
+        return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme (or at most %d overrides per symbol) and max word length <= %d (have %d%s)",
+                    NWAP_MAX_OV, NWAP_MAXLEN_FAST, c->qmax, c->general ? ", dense similarity table" : "");
 
     if (variant == NWAP_VARIANT_SIMPLE) {
         nwap_simple_params p;
@@ -146,7 +150,8 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
         return NWAP_OK;
     }
 
-    const int flavor = variant == NWAP_VARIANT_PACKED3 ? 1 : 0;
+    const bool ov = c->general;                       // here: general implies sparse_ov
+    const int flavor = (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
     const int qclass = c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
     nwap_tile_params p;
     p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad;
@@ -159,8 +164,9 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.sc = nwap_make_consts(c->match, c->mismatch, c->gap);
     p.stats = c->d_stats; p.want_hist = want_hist;
     p.unit_counter = c->d_counter;
+    p.ov_table = ov ? c->d_ov : nullptr; p.ov_K = ov ? c->K : 0;
 
-    const int occ = std::max(1, c->occ_tiles[flavor * 3 + qclass]);
+    const int occ = std::max(1, c->occ_tiles[(ov ? 2 : flavor) * 3 + qclass]);
     const int64_t slots = (int64_t)c->sm_count * occ;
     // bands per group: as large as possible (amortises the per-unit sort) while
     // leaving >= 24 units per resident CTA for dynamic balance.
@@ -179,7 +185,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.us = us; p.unit_begin = ubeg; p.unit_count = ucount;
     const int64_t grid = std::min<int64_t>(slots, ucount);
     CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
-    tile_kernel(flavor, qclass)<<<(unsigned)grid, NWAP_THREADS, sizeof(nwap_tile_smem), st>>>(p);
+    tile_kernel(flavor, qclass, ov)<<<(unsigned)grid, NWAP_THREADS, tile_smem(ov), st>>>(p);
     g_launches++;
     CK(cudaGetLastError());
     return NWAP_OK;
@@ -269,12 +275,13 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
         rc = build_sim_table(c, sim.data());
     }
     if (rc == NWAP_OK) {
-        for (int f = 0; f < 2 && rc == NWAP_OK; ++f)
+        for (int f = 0; f < 3 && rc == NWAP_OK; ++f)          // f == 2: sparse-override build
             for (int w = 0; w < 3 && rc == NWAP_OK; ++w) {
-                tile_kernel_t k = tile_kernel(f, w);
-                guard(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(nwap_tile_smem)), "cudaFuncSetAttribute");
+                tile_kernel_t k = tile_kernel(f == 2 ? 1 : f, w, f == 2);
+                const size_t smem = tile_smem(f == 2);
+                guard(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cudaFuncSetAttribute");
                 int occ = 0;
-                guard(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, sizeof(nwap_tile_smem)), "occupancy query");
+                guard(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem), "occupancy query");
                 c->occ_tiles[f * 3 + w] = occ;
             }
     }
@@ -300,6 +307,14 @@ int nwap_set_similarity(nwap_ctx *c, const int8_t *sim, int K)
     CK(cudaSetDevice(c->device));
     c->K = K;
     c->general = true;
+    // uniform + sparse corrections?  then the packed kernel can run it
+    std::vector<nwap_ov_row> tab((size_t)K);
+    c->sparse_ov = K <= NWAP_OV_MAXK && nwap_build_ov_table(sim, K, c->match, c->mismatch, tab.data());
+    if (c->d_ov) { cudaFree(c->d_ov); c->d_ov = nullptr; }
+    if (c->sparse_ov) {
+        CK(cudaMalloc(&c->d_ov, sizeof(nwap_ov_row) * (size_t)K));
+        CK(cudaMemcpy(c->d_ov, tab.data(), sizeof(nwap_ov_row) * (size_t)K, cudaMemcpyHostToDevice));
+    }
     return build_sim_table(c, sim);
 }
 
@@ -307,7 +322,7 @@ void nwap_destroy(nwap_ctx *c)
 {
     if (!c) return;
     cudaSetDevice(c->device);
-    cudaFree(c->d_ids); cudaFree(c->d_lens); cudaFree(c->d_sim); cudaFree(c->d_stats);
+    cudaFree(c->d_ids); cudaFree(c->d_lens); cudaFree(c->d_sim); cudaFree(c->d_stats); cudaFree(c->d_ov);
     cudaFree(c->d_counter); cudaFree(c->d_block_counts); cudaFree(c->d_total);
     cudaFree(c->d_slab[0]); cudaFree(c->d_slab[1]);
     for (int i = 0; i < 2; ++i) {

@@ -197,6 +197,86 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
 #endif
 }
 
+// ---- sparse overrides (ScoringScheme.overrides, reference aligner.py:51-65) -----------------
+// sim(a, b) = uniform(a, b) + delta(a, b) with delta != 0 for at most NWAP_MAX_OV partners b of
+// any symbol a.  For a matrix row whose symbol has partners (b_k, delta_k) the diagonal term is
+//     dw = diag - e*D + sum_k delta_k * [b_j == b_k]
+//        = diag - e*D + sum_k (delta_k - delta_k * e_k),   e_k = min(b_k + (-b_j), 1)
+// i.e. one extra DPX compare + IMAD per partner slot and one add of dsum = sum_k delta_k.
+// Rows whose symbol has no partner run the plain cell.
+#define NWAP_MAX_OV 3
+struct nwap_ov_row {                 // one row of the per-symbol override table
+    uint32_t b2[NWAP_MAX_OV];        // partner symbol * 65537 (unused slot: anything)
+    uint32_t nd[NWAP_MAX_OV];        // (uint32)(-delta_k)     (unused slot: 0)
+    uint32_t dsum;                   // (uint32)(sum_k delta_k) * 65537 ... packed for both halves
+    uint32_t count;                  // number of used slots
+};
+struct nwap_sym4 { uint32_t a2, left0, ovi, pad; };   // ovi = symbol index into the table, or NWAP_NO_OV
+#define NWAP_NO_OV 0xffffffffu
+
+template <int LB, int FLAVOR>
+NWAP_HD void nwap_dp_row_ov(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                            uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc, const nwap_ov_row &ov)
+{
+    uint32_t left = left0;
+    uint32_t diag = d0;
+#pragma unroll
+    for (int j = 1; j <= LB; ++j) {
+        uint32_t dw = nwap_viaddmin_u16x2(a2, nb[j - 1], 0x00010001u) * sc.neg_delta + diag;
+#pragma unroll
+        for (int k = 0; k < NWAP_MAX_OV; ++k)
+            dw = nwap_viaddmin_u16x2(ov.b2[k], nb[j - 1], 0x00010001u) * ov.nd[k] + dw;
+        dw += ov.dsum;
+        diag = P[j];
+        const uint32_t upu = P[j] + sc.u2;
+        const uint32_t cur = nwap_vimax3_s16x2(dw, upu, left);
+        P[j] = cur;
+        left = cur;
+    }
+}
+
+template <int LB, int FLAVOR>
+NWAP_HD void nwap_dp_word_ov(const nwap_sym4 *row_sym4, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                             const nwap_scheme_consts &sc, const nwap_ov_row *ovtab)
+{
+#pragma unroll
+    for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
+    uint32_t d0 = NWAP_BIAS2;
+    const nwap_sym4 *s = row_sym4, *e = row_sym4 + la;
+#pragma unroll 1
+    do {
+        const nwap_sym4 x = *s++;
+        if (x.ovi == NWAP_NO_OV) nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+        else nwap_dp_row_ov<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc, ovtab[x.ovi]);
+        d0 = x.left0;
+    } while (s != e);
+}
+
+// Host-side construction of the override table from a dense K x K similarity table
+// (reference engine.py:110-117).  Returns false when some symbol has more than NWAP_MAX_OV
+// partners (the scheme then goes to the table-driven generic kernel).
+inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatch, nwap_ov_row *out)
+{
+    for (int a = 0; a < K; ++a) {
+        nwap_ov_row r;
+        for (int k = 0; k < NWAP_MAX_OV; ++k) { r.b2[k] = 0; r.nd[k] = 0; }
+        int cnt = 0, dsum = 0;
+        for (int b = 0; b < K; ++b) {
+            const int delta = (int)sim[a * K + b] - (a == b ? match : mismatch);
+            if (delta == 0) continue;
+            if (cnt == NWAP_MAX_OV) return false;
+            r.b2[cnt] = (uint32_t)b * 65537u;
+            r.nd[cnt] = (uint32_t)(-delta);
+            dsum += delta;
+            ++cnt;
+        }
+        r.dsum = (uint32_t)(dsum * 65537);
+        r.count = (uint32_t)cnt;
+        out[a] = r;
+    }
+    return true;
+}
+
 // ---- dual chain: the same row word against TWO column pairs per lane (registers PA/PB) ----
 // Halves the per-matrix-row loop overhead and the per-row dispatch for short words; the two
 // chains are independent, which also doubles the ILP of the max-chain.

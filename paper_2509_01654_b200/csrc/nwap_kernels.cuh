@@ -58,6 +58,8 @@ struct nwap_tile_params {
     unsigned long long *unit_counter;
     nwap_dev_stats *stats;
     int want_hist;
+    const nwap_ov_row *ov_table;   // sparse-override mode: (ov_K) rows on the device, else NULL
+    int ov_K;
 };
 
 struct nwap_row_meta {
@@ -73,9 +75,16 @@ struct nwap_row_meta {
 // ---------------------------------------------------------------------------
 // shared memory carve-up of k_score_tiles
 // ---------------------------------------------------------------------------
-struct nwap_tile_smem {
+#define NWAP_OV_MAXK 128               // largest alphabet the sparse-override table holds in shared memory
+template <bool OV> struct nwap_sym_of { typedef nwap_sym2 type; };
+template <> struct nwap_sym_of<true> { typedef nwap_sym4 type; };
+
+template <bool OV>
+struct nwap_tile_smem_t {
     alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
-    alignas(16) nwap_sym2 rowsym[NWAP_R][NWAP_MAXLEN_FAST + 1];  // {a*65537, H'[i+1][0]} per matrix row (+1 pad)
+    typedef typename nwap_sym_of<OV>::type sym_t;
+    alignas(16) sym_t rowsym[NWAP_R][NWAP_MAXLEN_FAST + 1];      // {a*65537, H'[i+1][0] (, override row)} per matrix row
+    alignas(16) nwap_ov_row ov[OV ? NWAP_OV_MAXK : 1];              // per-symbol override table (sparse-override mode)
     nwap_row_meta meta[NWAP_R];
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
     uint8_t clen[NWAP_C];         // their lengths
@@ -90,6 +99,8 @@ struct nwap_tile_smem {
     int band_simple;      // every staged row is valid over the whole sorted column window
     int n_long_chunks;    // leading 64-column chunks that hold words longer than NWAP_DUAL_MAX
 };
+
+typedef nwap_tile_smem_t<false> nwap_tile_smem;
 
 __device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
 {
@@ -127,7 +138,8 @@ __device__ __forceinline__ nwap_lane_cols nwap_make_lane_cols(uint32_t off0, uin
 struct nwap_chunk_acc { uint32_t acc, acc_hi; int rows_fast; };
 
 // Score fix-up, staging store and statistics of one packed result (shared by all lengths).
-__device__ __forceinline__ void nwap_emit(nwap_tile_smem &sm, const nwap_row_meta &m, uint32_t v,
+template <class SM>
+__device__ __forceinline__ void nwap_emit(SM &sm, const nwap_row_meta &m, uint32_t v,
                                           const nwap_lane_cols &c, bool fast, int want_hist,
                                           nwap_lane_stats &ls, nwap_chunk_acc &ca)
 {
@@ -181,12 +193,27 @@ struct nwap_false { __device__ constexpr operator bool() const { return false; }
 // final cells for words of length LB (v) and LB-1 (vm1) -- all a sorted chunk normally
 // contains; `deep` (a chunk spanning three or more lengths: the long and short tails of a
 // strip) selects per lane among all columns.
+__device__ __forceinline__ void nwap_dp_word_any(const nwap_sym2 *, const nwap_ov_row *) {}
 template <int LB, int FLAVOR>
-__device__ __forceinline__ void nwap_row_dp(const nwap_sym2 *sym, int la, const uint32_t *nb, int l0, int l1,
-                                            const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1, bool deep)
+__device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym2 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                                                 const nwap_scheme_consts &sc, const nwap_ov_row *)
+{
+    nwap_dp_word<LB, FLAVOR>(sym, la, nb, P, sc);
+}
+template <int LB, int FLAVOR>
+__device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym4 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                                                 const nwap_scheme_consts &sc, const nwap_ov_row *ovtab)
+{
+    nwap_dp_word_ov<LB, FLAVOR>(sym, la, nb, P, sc, ovtab);
+}
+
+template <int LB, int FLAVOR, class SYM>
+__device__ __forceinline__ void nwap_row_dp(const SYM *sym, const nwap_ov_row *ovtab, int la, const uint32_t *nb,
+                                            int l0, int l1, const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1,
+                                            bool deep)
 {
     uint32_t P[LB + 1];
-    nwap_dp_word<LB, FLAVOR>(sym, la, nb, P, sc);
+    nwap_dp_word_sel<LB, FLAVOR>(sym, la, nb, P, sc, ovtab);
     v = P[LB];
     vm1 = P[LB >= 2 ? LB - 1 : LB];
     if (deep) {
@@ -235,8 +262,8 @@ __device__ __forceinline__ void nwap_row_dp2(const nwap_sym2 *sym, int la, const
 // usual case at a bucket boundary of the sorted strip); 2 = anything.  fast: the chunk is full
 // and every staged row is valid over the whole column window, so no per-lane range checks are
 // needed (the overwhelmingly common case).  All warp-uniform.
-template <int FLAVOR, int QMAX, int QW>
-__device__ __forceinline__ void nwap_run_chunk(int LB, nwap_tile_smem &sm, const nwap_scheme_consts &sc,
+template <int FLAVOR, int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme_consts &sc,
                                                const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
                                                const nwap_lane_cols &c, int mixmode, bool fast,
                                                int want_hist, nwap_lane_stats &ls)
@@ -252,11 +279,11 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, nwap_tile_smem &sm, const
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
         if (la == 0) continue;                       // uniform across the CTA
-        const nwap_sym2 *sym = sm.rowsym[rr];
+        const typename SM::sym_t *sym = sm.rowsym[rr];
         uint32_t v = 0, vm1 = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
-        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, la, nb, l0, l1, sc, v, vm1, deep);    \
+        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, sm.ov, la, nb, l0, l1, sc, v, vm1, deep); \
         break;
         switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
@@ -273,8 +300,8 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, nwap_tile_smem &sm, const
 #ifndef NWAP_DUAL_MAX
 #define NWAP_DUAL_MAX 0
 #endif
-template <int FLAVOR, int QW>
-__device__ __forceinline__ void nwap_run_chunk2(int LB, nwap_tile_smem &sm, const nwap_scheme_consts &sc,
+template <int FLAVOR, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk2(int LB, SM &sm, const nwap_scheme_consts &sc,
                                                 const uint32_t (&wa0)[QW], const uint32_t (&wa1)[QW],
                                                 const uint32_t (&wb0)[QW], const uint32_t (&wb1)[QW],
                                                 const nwap_lane_cols &cA, const nwap_lane_cols &cB,
@@ -294,7 +321,7 @@ __device__ __forceinline__ void nwap_run_chunk2(int LB, nwap_tile_smem &sm, cons
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
         if (la == 0) continue;
-        const nwap_sym2 *sym = sm.rowsym[rr];
+        const nwap_sym2 *sym = reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]);   // dual chains: non-override builds only
         uint32_t vA = 0, vAm1 = 0, vB = 0, vBm1 = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
@@ -313,14 +340,25 @@ __device__ __forceinline__ void nwap_run_chunk2(int LB, nwap_tile_smem &sm, cons
     nwap_close_chunk(ls, ca);
 }
 
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, uint32_t left0, const nwap_ov_row *, int)
+{
+    x.a2 = a * 65537u; x.left0 = left0;
+}
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_t left0, const nwap_ov_row *ov, int K)
+{
+    x.a2 = a * 65537u; x.left0 = left0; x.pad = 0;
+    x.ovi = ((int)a < K && ov[a].count) ? a : NWAP_NO_OV;
+}
+
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
 // accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
-template <int FLAVOR, int QMAX>
-__global__ void __launch_bounds__(NWAP_THREADS, (QMAX <= 24 ? NWAP_MINB : (NWAP_MINB > 4 ? 4 : NWAP_MINB)))
+template <int FLAVOR, int QMAX, bool OV>
+__global__ void __launch_bounds__(NWAP_THREADS, (OV ? 4 : (QMAX <= 24 ? NWAP_MINB : (NWAP_MINB > 4 ? 4 : NWAP_MINB))))
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    nwap_tile_smem &sm = *reinterpret_cast<nwap_tile_smem *>(smem_raw);
+    typedef nwap_tile_smem_t<OV> smem_t;
+    smem_t &sm = *reinterpret_cast<smem_t *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const nwap_scheme_consts sc = p.sc;
     constexpr int MAXL = QMAX;
@@ -328,6 +366,11 @@ k_score_tiles(const nwap_tile_params p)
 
     if (tid == 0) { sm.sum = 0; sm.count = 0; sm.mn = 127; sm.mx = -128; }
     for (int b = tid; b < 256; b += NWAP_THREADS) sm.hist[b] = 0;
+    if (OV) {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(p.ov_table);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(sm.ov);
+        for (int w = tid; w < p.ov_K * (int)(sizeof(nwap_ov_row) / 4); w += NWAP_THREADS) dst[w] = src[w];
+    }
     nwap_lane_stats ls;
     ls.mn2 = 0x7fff7fffu; ls.mx2 = 0u; ls.sum = 0; ls.count = 0;
 
@@ -430,10 +473,9 @@ k_score_tiles(const nwap_tile_params p)
                     const uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(p.ids + r * p.qpad) + q4);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        nwap_sym2 x;
-                        x.a2 = ((v >> (8 * e)) & 0xffu) * 65537u;
-                        x.left0 = NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2;
-                        sm.rowsym[rr][q4 * 4 + e] = x;
+                        const uint32_t a = (v >> (8 * e)) & 0xffu;
+                        nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
+                                       sm.ov, p.ov_K);
                     }
                 }
             }
@@ -479,7 +521,7 @@ k_score_tiles(const nwap_tile_params p)
                     w1[4 * v] = y.x; w1[4 * v + 1] = y.y; w1[4 * v + 2] = y.z; w1[4 * v + 3] = y.w;
                 }
                 const nwap_lane_cols cA = nwap_make_lane_cols(off0, off1, la_, lb_, LB, sc);
-                if (!dual) {
+                if (OV || !dual) {
                     const int lmin = min(la_, lb_);
                     const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
                                       : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;

@@ -59,7 +59,52 @@ static void run_quad(const uint8_t *a, int la, const uint8_t *const b[4], const 
     scores[3] = nwap_unbias(ob >> 16, la, lb[3], sc);
 }
 
+template <int LB>
+static uint32_t run_pair_ov(const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,
+                            const nwap_scheme_consts &sc, const nwap_ov_row *tab)
+{
+    nwap_sym4 row4[256];
+    for (int i = 0; i < la; ++i) {
+        row4[i].a2 = (uint32_t)a[i] * 65537u;
+        row4[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+        row4[i].ovi = tab[a[i]].count ? a[i] : NWAP_NO_OV;
+        row4[i].pad = 0;
+    }
+    uint32_t nb[LB];
+    for (int j = 0; j < LB; ++j) nb[j] = nwap_pack_negb(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
+    uint32_t P[LB + 1];
+    nwap_dp_word_ov<LB, 1>(row4, la, nb, P, sc, tab);
+    uint32_t lo = 0, hi = 0;
+    for (int j = 1; j <= LB; ++j) {
+        if (j == lb0) lo = P[j] & 0xffffu;
+        if (j == lb1) hi = P[j] >> 16;
+    }
+    return lo | (hi << 16);
+}
+
 extern "C" {
+
+// Sparse-override mode: sim is a dense K x K int8 table; returns -2 when it is not sparse enough.
+int emul_pair_scores_ov(int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,
+                        const int8_t *sim, int K, int match, int mismatch, int gap, int *s0, int *s1)
+{
+    if (LB < 1 || LB > 32 || lb0 > LB || lb1 > LB || la < 1 || K > 256) return -1;
+    static nwap_ov_row tab[256];
+    if (!nwap_build_ov_table(sim, K, match, mismatch, tab)) return -2;
+    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap);
+    uint32_t v = 0;
+    switch (LB) {
+#define CASE(n) case n: v = run_pair_ov<n>(a, la, b0, lb0, b1, lb1, sc, tab); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+        CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24)
+        CASE(25) CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
+#undef CASE
+    }
+    *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
+    *s1 = nwap_unbias(v >> 16, la, lb1, sc);
+    return 0;
+}
 
 // Dual chain: (a vs b0..b3) at register width LB (<= 16 here).
 int emul_quad_scores(int flavor, int LB, const uint8_t *a, int la, const uint8_t *b0, const uint8_t *b1,

@@ -27,6 +27,8 @@ def emul():
     L = ctypes.CDLL(str(SO))
     p, i, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
     L.emul_pair_scores.argtypes = [i, i, p, i, p, i, p, i, i, i, i, p, p]
+    L.emul_pair_scores_ov.argtypes = [i, p, i, p, i, p, i, p, i, i, i, i, p, p]
+    L.emul_quad_scores.argtypes = [i, i, p, i, p, p, p, p, p, i, i, i, p]
     L.emul_row_of.restype = i64
     L.emul_row_of.argtypes = [i64, i64]
     L.emul_col_of.restype = i64
@@ -84,6 +86,60 @@ def test_packed_recurrence_extreme_schemes(emul):
                 emul.emul_pair_scores(fl, max(lb0, lb1), a.ctypes.data, la, b0.ctypes.data, lb0,
                                       b1.ctypes.data, lb1, m, x, g, ctypes.addressof(s0), ctypes.addressof(s1))
                 assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim, g), orc.c_nw_score(a, b1, sim, g))
+
+
+def test_sparse_override_rows_match_oracle(emul):
+    """ScoringScheme.overrides (aligner.py:51-65) as sparse corrections of the packed cell."""
+    rng = random.Random(11)
+    checked = dense = 0
+    for _ in range(4000):
+        q, K = rng.randint(1, 24), rng.choice([3, 5, 8, 40])
+        while True:
+            m, x, g = rng.randint(-2, 4), rng.randint(-4, 3), rng.randint(-4, 2)
+            ov = {}
+            for _k in range(rng.randint(0, 4)):
+                a_, b_ = rng.randrange(K), rng.randrange(K)
+                ov[(min(a_, b_), max(a_, b_))] = rng.randint(-4, 4)
+            vals = [m, x, *ov.values()]
+            if min(0, 2 * q * g, q * min(vals)) >= -128 and max(0, 2 * q * g, q * max(vals)) <= 127:
+                break
+        la, lb0, lb1 = rng.randint(1, q), rng.randint(1, q), rng.randint(1, q)
+        LB = rng.randint(max(lb0, lb1), q)
+        a = np.array([rng.randrange(K) for _ in range(la)], dtype=np.uint8)
+        b0 = np.array([rng.randrange(K) for _ in range(lb0)], dtype=np.uint8)
+        b1 = np.array([rng.randrange(K) for _ in range(lb1)], dtype=np.uint8)
+        sim = orc.similarity_matrix(m, x, K, ov)
+        sim8 = np.ascontiguousarray(sim.astype(np.int8))
+        s0, s1 = ctypes.c_int(), ctypes.c_int()
+        rc = emul.emul_pair_scores_ov(LB, a.ctypes.data, la, b0.ctypes.data, lb0, b1.ctypes.data, lb1,
+                                      sim8.ctypes.data, K, m, x, g, ctypes.addressof(s0), ctypes.addressof(s1))
+        if rc == -2:
+            dense += 1
+            continue
+        assert rc == 0
+        checked += 1
+        assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim, g), orc.c_nw_score(a, b1, sim, g)), (m, x, g, ov)
+    assert checked > 3500 and dense < 100
+
+
+def test_dual_chain_matches_oracle(emul):
+    rng = random.Random(5)
+    for _ in range(3000):
+        q = rng.randint(1, 16)
+        m, x, g = _random_scheme(rng, q)
+        K = rng.choice([2, 3, 5, 40])
+        la = rng.randint(1, q)
+        lb = [rng.randint(1, q) for _ in range(4)]
+        LB = rng.randint(max(lb), q)
+        a = np.array([rng.randrange(K) for _ in range(la)], dtype=np.uint8)
+        bs = [np.array([rng.randrange(K) for _ in range(l)], dtype=np.uint8) for l in lb]
+        sim = orc.similarity_matrix(m, x, 64)
+        lbarr = np.array(lb, dtype=np.int32)
+        out = np.zeros(4, dtype=np.int32)
+        for fl in (0, 1):
+            assert emul.emul_quad_scores(fl, LB, a.ctypes.data, la, *[b.ctypes.data for b in bs],
+                                         lbarr.ctypes.data, m, x, g, out.ctypes.data) == 0
+            assert list(out) == [orc.c_nw_score(a, b, sim, g) for b in bs]
 
 
 def test_device_index_recovery_matches_reference(emul, golden_triangle):

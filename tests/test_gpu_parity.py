@@ -144,7 +144,8 @@ def test_golden_engine_cases(golden_cases, name):
     n = len(c["lengths"])
     P = nw.num_edges(n)
     with NwapContext(c["ids"], c["lengths"], scheme) as ctx:
-        variants = ["simple"] if (c.get("overrides") or ctx.max_len > 32) else ALL
+        # sparse overrides run on the packed kernel too; q > 32 only on the generic one
+        variants = ["simple"] if ctx.max_len > 32 else (["packed3", "simple"] if c.get("overrides") else ALL)
         for v in variants + ["auto"]:
             got, st = _score(ctx, 0, P, v, want_hist=True)
             assert np.array_equal(got, c["payload"]), (name, v)
@@ -211,6 +212,49 @@ def test_random_schemes_all_variants():
             for v in ALL:
                 got, _ = _score(ctx, 0, P, v)
                 assert np.array_equal(got, ref), (trial, v, (m, x, g), q)
+
+
+def test_sparse_override_schemes_on_the_packed_kernel():
+    """ScoringScheme.overrides: random sparse override sets (<= 3 partners per symbol) must give the same
+    bytes on the packed sparse-override kernel, the generic kernel and the oracle; a dense table is
+    refused by the packed kernel and served by the generic one."""
+    rng = np.random.default_rng(77)
+    for trial in range(10):
+        q = int(rng.integers(4, 25))
+        K = int(rng.integers(3, 41))
+        while True:
+            m, x, g = int(rng.integers(0, 4)), int(rng.integers(-4, 1)), int(rng.integers(-4, 0))
+            ov = {}
+            for _ in range(int(rng.integers(1, 6))):
+                a_, b_ = int(rng.integers(0, K)), int(rng.integers(0, K))
+                ov[(min(a_, b_), max(a_, b_))] = int(rng.integers(-4, 5))
+            vals = [m, x, *ov.values()]
+            if min(0, 2 * q * g, q * min(vals)) >= -128 and max(0, 2 * q * g, q * max(vals)) <= 127:
+                break
+        n = int(rng.integers(300, 2600))
+        lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
+        lens[0] = q
+        ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
+        scheme = nw.ScoringScheme(m, x, g, overrides=ov)
+        P = nw.num_edges(n)
+        ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P, threads=4)
+        with NwapContext(ids, lens, scheme) as ctx:
+            for v in ("auto", "packed3", "simple"):
+                got, st = _score(ctx, 0, P, v, want_hist=(trial % 2 == 0))
+                assert np.array_equal(got, ref), (trial, v, (m, x, g), ov)
+                assert st[:4] == (rsum, rmin, rmax, P)
+    # dense table: every pair overridden
+    K, n, q = 6, 200, 8
+    ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
+    lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
+    ov = {(a, b): int((a * 7 + b * 3) % 5 - 2) for a in range(K) for b in range(a, K)}
+    scheme = nw.ScoringScheme(1, -1, -2, overrides=ov)
+    ref, *_ = _oracle(ids, lens, scheme, 0, nw.num_edges(n))
+    with NwapContext(ids, lens, scheme) as ctx:
+        got, _ = _score(ctx, 0, nw.num_edges(n), "auto")
+        assert np.array_equal(got, ref)
+        with pytest.raises(ValueError, match="packed kernel"):
+            ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed3")
 
 
 # ---- BASELINE.json configs -------------------------------------------------------------------
