@@ -44,9 +44,12 @@ BASE_N = 100_000
 SM_COUNT = 148
 
 
-def workload(n_gpus: int, n_words: int | None):
+def workload(n_gpus: int, n_words: int | None, fixed_len: int = 0):
     n = n_words if n_words else int(round(BASE_N * math.sqrt(n_gpus)))
     ids, lens = synth.french_shaped(n)
+    if fixed_len:      # diagnostic only: every word the same length (isolates length-mix effects)
+        lens = np.full(n, fixed_len, dtype=np.uint8)
+        ids = np.random.default_rng(1).integers(0, synth.ALPHABET, size=(n, fixed_len)).astype(np.uint8)
     scheme = synth.CONFIG_SCHEMES["C3"]
     name = (f"synthetic French-shaped vocabulary, n={n} words (configs[2] shape: length~clip(round(N(8.5,2.8)),1,24), "
             f"alphabet 40), scheme match/mismatch/gap={scheme}, all {n * (n - 1) // 2} pairs, int8 condensed output")
@@ -196,6 +199,7 @@ def main():
     ap.add_argument("--words", type=int, default=0, help="override vocabulary size (default 100000*sqrt(gpus))")
     ap.add_argument("--variant", default="auto", choices=["auto", "packed", "packed3", "simple"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the CPU baseline sample")
+    ap.add_argument("--fixed-len", type=int, default=0, help="diagnostic: all words of this length")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -206,7 +210,7 @@ def main():
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
 
-    ids, lens, scheme, wname = workload(args.gpus, args.words)
+    ids, lens, scheme, wname = workload(args.gpus, args.words, args.fixed_len)
     n = len(lens)
     P = n * (n - 1) // 2
     cells_total = synth.total_cells(lens)

@@ -139,13 +139,12 @@ struct nwap_chunk_acc { uint32_t acc, acc_hi; int rows_fast; };
 
 // Score fix-up, staging store and statistics of one packed result (shared by all lengths).
 template <class SM>
-__device__ __forceinline__ void nwap_emit(SM &sm, const nwap_row_meta &m, uint32_t v,
+__device__ __forceinline__ void nwap_emit(SM &sm, const nwap_row_meta &m, uint32_t ala2, int adj, uint32_t v,
                                           const nwap_lane_cols &c, bool fast, int want_hist,
                                           nwap_lane_stats &ls, nwap_chunk_acc &ca)
 {
-    const uint32_t t = v + m.ala2 + c.kpos2;        // halves: score + BIAS (never negative)
+    const uint32_t t = v + ala2 + c.kpos2;          // halves: score + BIAS (never negative)
     const uint32_t thi = t >> 16;
-    const int adj = m.rowadj;
     if (fast) {
         sm.out[adj + (int)c.off0] = (uint8_t)t;
         sm.out[adj + (int)c.off1] = (uint8_t)thi;
@@ -288,8 +287,50 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
         switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
         if (mixmode == 1) v = (v & c.keep_v) | (vm1 & ~c.keep_v);
-        nwap_emit(sm, m, v, c, fast, want_hist, ls, ca);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
     }
+    nwap_close_chunk(ls, ca);
+}
+
+// NWAP_HOIST=1 (A/B): the length dispatch is done once per chunk and each length body owns the
+// whole row loop (fast emit inlined, slow emit shared through a flag).
+#ifndef NWAP_HOIST
+#define NWAP_HOIST 0
+#endif
+template <int LB, int FLAVOR, class SM>
+__device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
+                                                  const nwap_lane_cols &c, int mixmode, bool fast, int want_hist,
+                                                  nwap_lane_stats &ls, nwap_chunk_acc &ca)
+{
+    const bool deep = mixmode > 1;
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;
+        uint32_t v, vm1;
+        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, deep);
+        if (mixmode == 1) v = (v & c.keep_v) | (vm1 & ~c.keep_v);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+}
+
+template <int FLAVOR, int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                 const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                 const nwap_lane_cols &c, int mixmode, bool fast,
+                                                 int want_hist, nwap_lane_stats &ls)
+{
+    uint32_t nb[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_chunk_rows_h<(n <= QMAX ? n : 1), FLAVOR>(sm, sc, nb, c, mixmode, fast, want_hist, ls, ca); \
+        break;
+    switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
     nwap_close_chunk(ls, ca);
 }
 
@@ -333,8 +374,8 @@ __device__ __forceinline__ void nwap_run_chunk2(int LB, SM &sm, const nwap_schem
             vA = (vA & cA.keep_v) | (vAm1 & ~cA.keep_v);
             vB = (vB & cB.keep_v) | (vBm1 & ~cB.keep_v);
         }
-        nwap_emit(sm, m, vA, cA, fast, want_hist, ls, ca);
-        nwap_emit(sm, m, vB, cB, fast, want_hist, ls, ca);
+        nwap_emit(sm, m, m.ala2, m.rowadj, vA, cA, fast, want_hist, ls, ca);
+        nwap_emit(sm, m, m.ala2, m.rowadj, vB, cB, fast, want_hist, ls, ca);
     }
     // two emits per row: rows_fast counted twice, which is what nwap_close_chunk expects (2 scores each)
     nwap_close_chunk(ls, ca);
@@ -526,7 +567,11 @@ k_score_tiles(const nwap_tile_params p)
                     const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
                                       : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
                     const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
+#if NWAP_HOIST
+                    nwap_run_chunk_h<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+#else
                     nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+#endif
                 } else {
                     const int kc2 = kc + NWAP_CHUNK;
                     const int kd = kc2 + 2 * lane, ke = kd + 1;
