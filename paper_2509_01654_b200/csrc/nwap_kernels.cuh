@@ -334,6 +334,114 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
     nwap_close_chunk(ls, ca);
 }
 
+// ---------------------------------------------------------------------------
+// STREAM path (NWAP_STREAM=1): the 16 row words of a simple band are one symbol stream in shared
+// memory -- rowsym[rr][0..la) are the matrix rows of word rr and rowsym[rr][la] is a BOUNDARY record
+// {alpha*la*65537, left0 = 0}.  A chunk then needs ONE length dispatch and ONE loop: at a boundary the
+// length-specialised body itself stores the two score bytes, updates the packed statistics,
+// re-initialises the rolling row and jumps to the next word.  No per-row dispatch, no per-row
+// prologue.  Lanes beyond the end of the sorted list recompute the chunk's first column; their stores
+// are predicated off (st0/st1) and their sums masked (vmask); min/max may see the duplicates.
+// ---------------------------------------------------------------------------
+// A/B-tested and REJECTED (profiles/r01e_ab_stream_hoist.txt): +9 % at L = 4 but -5..-8 % at L >= 8
+// (four extra moves + a test per matrix row) and -4 % / -19 % on the 100k / 20k French-shaped
+// workloads (a second code family next to the per-row path).  Compiled out by default.
+#ifndef NWAP_STREAM
+#define NWAP_STREAM 0
+#endif
+
+// one matrix row from a stream record, plain or sparse-override
+template <int LB, int FLAVOR>
+__device__ __forceinline__ void nwap_dp_row_any(const nwap_sym2 &x, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                                                uint32_t d0, const nwap_scheme_consts &sc, const nwap_ov_row *)
+{
+    nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+}
+template <int LB, int FLAVOR>
+__device__ __forceinline__ void nwap_dp_row_any(const nwap_sym4 &x, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                                                uint32_t d0, const nwap_scheme_consts &sc, const nwap_ov_row *ovtab)
+{
+    if (x.ovi == NWAP_NO_OV) nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+    else nwap_dp_row_ov<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc, ovtab[x.ovi]);
+}
+
+template <int LB, int FLAVOR, class SM>
+__device__ __forceinline__ void nwap_chunk_stream(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
+                                                  const nwap_lane_cols &c, int mixmode, bool st0, bool st1,
+                                                  uint32_t vmask, nwap_lane_stats &ls, uint32_t &acc, uint32_t &acc_hi)
+{
+    typedef typename SM::sym_t sym_t;
+    uint32_t P[LB + 1];
+#pragma unroll
+    for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
+    uint32_t d0 = NWAP_BIAS2;
+    int rr = 0;
+    const sym_t *s = sm.rowsym[0];
+#pragma unroll 1
+    for (;;) {
+        const sym_t x = *s++;
+        if (x.left0 != 0u) {
+            nwap_dp_row_any<LB, FLAVOR>(x, nb, P, d0, sc, sm.ov);
+            d0 = x.left0;
+            continue;
+        }
+        // ---- boundary: the word of band row rr is finished; x.a2 is its packed row potential ----
+        uint32_t v = P[LB];
+        if (mixmode) {
+            if (mixmode == 1) {
+                v = (v & c.keep_v) | (P[LB >= 2 ? LB - 1 : LB] & ~c.keep_v);
+            } else {
+                uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
+#pragma unroll
+                for (int j = 1; j < LB; ++j) {
+                    if (j == c.l0) lo = P[j] & 0xffffu;
+                    if (j == c.l1) hi = P[j] & 0xffff0000u;
+                }
+                v = lo | hi;
+            }
+        }
+        const uint32_t t = v + x.a2 + c.kpos2;       // halves: score + BIAS
+        const uint32_t thi = t >> 16;
+        const int adj = sm.meta[rr].rowadj;
+        if (st0) sm.out[adj + (int)c.off0] = (uint8_t)t;
+        if (st1) sm.out[adj + (int)c.off1] = (uint8_t)thi;
+        ls.mn2 = __vmins2(ls.mn2, t);
+        ls.mx2 = __vmaxs2(ls.mx2, t);
+        const uint32_t tm = t & vmask;
+        acc += tm;
+        acc_hi += tm >> 16;
+        if (++rr == NWAP_R) break;
+        s = sm.rowsym[rr];
+#pragma unroll
+        for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
+        d0 = NWAP_BIAS2;
+    }
+}
+
+template <int FLAVOR, int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk_stream(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                      const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                      const nwap_lane_cols &c, int mixmode, bool va, bool vb,
+                                                      nwap_lane_stats &ls)
+{
+    uint32_t nb[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    const uint32_t vmask = (va ? 0xffffu : 0u) | (vb ? 0xffff0000u : 0u);
+    uint32_t acc = 0, acc_hi = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_chunk_stream<(n <= QMAX ? n : 1), FLAVOR>(sm, sc, nb, c, mixmode, va, vb, vmask, ls, acc, acc_hi); \
+        break;
+    switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+    // acc = sum(lo) + 65536 * sum(hi) (mod 2^32), acc_hi = sum(hi); all R rows of a simple band are present
+    const int nvalid = (va ? 1 : 0) + (vb ? 1 : 0);
+    const uint32_t sum_lo = acc - (acc_hi << 16);
+    ls.sum += (long long)sum_lo + (long long)acc_hi - (long long)(NWAP_R * nvalid) * (long long)NWAP_BIAS;
+    ls.count += NWAP_R * nvalid;
+}
+
 // Dual-chain chunk: 128 sorted columns (4 per lane), every word no longer than NWAP_DUAL_MAX.
 // A/B-tested and REJECTED (profiles/r01d_ab_dual.txt: 8.8 vs 10.5 TCUPS at DUAL_MAX=12): inside
 // the DP loops the kernel is already DPX-pipe-bound, so halving the loop overhead buys nothing
@@ -389,6 +497,12 @@ __device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_
 {
     x.a2 = a * 65537u; x.left0 = left0; x.pad = 0;
     x.ovi = ((int)a < K && ov[a].count) ? a : NWAP_NO_OV;
+}
+
+__device__ __forceinline__ void nwap_stage_boundary(nwap_sym2 &x, uint32_t ala2) { x.a2 = ala2; x.left0 = 0u; }
+__device__ __forceinline__ void nwap_stage_boundary(nwap_sym4 &x, uint32_t ala2)
+{
+    x.a2 = ala2; x.left0 = 0u; x.ovi = NWAP_NO_OV; x.pad = 0u;
 }
 
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
@@ -505,6 +619,8 @@ k_score_tiles(const nwap_tile_params p)
                     }
                 }
                 sm.meta[tid] = m;
+                // boundary record of the symbol stream (read only on the STREAM path)
+                nwap_stage_boundary(sm.rowsym[tid][m.la], m.ala2);
             }
             // stage row symbols, packed a*65537, with the row boundary values (4 symbols per item)
             for (int item = tid; item < NWAP_R * (NWAP_MAXLEN_FAST / 4); item += NWAP_THREADS) {
@@ -512,11 +628,13 @@ k_score_tiles(const nwap_tile_params p)
                 const int64_t r = rb0 + rr;
                 if (q4 < QW && r >= rmin && r <= rmax) {
                     const uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(p.ids + r * p.qpad) + q4);
+                    const int la_r = (int)p.lens[r];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const uint32_t a = (v >> (8 * e)) & 0xffu;
-                        nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
-                                       sm.ov, p.ov_K);
+                        if (q4 * 4 + e < la_r)           // slot [la] belongs to the boundary record
+                            nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
+                                           sm.ov, p.ov_K);
                     }
                 }
             }
@@ -566,6 +684,15 @@ k_score_tiles(const nwap_tile_params p)
                     const int lmin = min(la_, lb_);
                     const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
                                       : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
+#if NWAP_STREAM
+                    if (band_simple) {
+                        nwap_lane_cols cS = cA;                // dummy lanes: any in-range offset (stores are predicated off)
+                        if (!va) cS.off0 = 0u;
+                        if (!vb) cS.off1 = 0u;
+                        nwap_run_chunk_stream<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cS, mixmode, va, vb, ls);
+                        continue;
+                    }
+#endif
                     const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
 #if NWAP_HOIST
                     nwap_run_chunk_h<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
