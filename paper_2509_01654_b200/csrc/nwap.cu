@@ -111,16 +111,6 @@ int fetch_stats(nwap_ctx *c, nwap_stats *out, cudaStream_t st)
     return NWAP_OK;
 }
 
-void merge_stats(nwap_stats *acc, const nwap_stats *s, int want_hist)
-{
-    acc->sum += s->sum;
-    acc->count += s->count;
-    acc->min = std::min(acc->min, s->min);
-    acc->max = std::max(acc->max, s->max);
-    if (want_hist)
-        for (int b = 0; b < 256; ++b) acc->hist[b] += s->hist[b];
-}
-
 // Enqueue the scoring of [start, end) into out_dev on `st`.  Statistics accumulate
 // into c->d_stats (caller resets).  No synchronisation.
 int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int want_hist,

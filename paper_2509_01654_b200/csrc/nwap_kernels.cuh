@@ -24,6 +24,9 @@
 #ifndef NWAP_COLD_FAMILY
 #define NWAP_COLD_FAMILY 0
 #endif
+#ifndef NWAP_LBSTEP
+#define NWAP_LBSTEP 1
+#endif
 #ifndef NWAP_MINB
 #define NWAP_MINB 5               // resident CTAs/SM the register allocator must allow (Q <= 24)
 #endif
@@ -121,7 +124,8 @@ struct nwap_lane_cols {
     uint32_t off0, off1;    // strip-relative column offsets (0xffff = no column)
     int l0, l1;             // word lengths
     uint32_t kpos2;         // column potentials, packed (BIAS stays in: halves of t are score + BIAS)
-    uint32_t keep_v;        // per-half mask: 0xffff where the word has length LB (else LB-1 in mixmode 1)
+    uint32_t keep_v;        // per-half mask: 0xffff where the word has length LB
+    uint32_t keep_1;        // per-half mask: 0xffff where the word has length LB-1 (else LB-2 in mixmode 2)
 };
 
 __device__ __forceinline__ nwap_lane_cols nwap_make_lane_cols(uint32_t off0, uint32_t off1, int l0, int l1, int LB,
@@ -131,6 +135,7 @@ __device__ __forceinline__ nwap_lane_cols nwap_make_lane_cols(uint32_t off0, uin
     c.off0 = off0; c.off1 = off1; c.l0 = l0; c.l1 = l1;
     c.kpos2 = (uint32_t)(sc.beta * l0) + ((uint32_t)(sc.beta * l1) << 16);
     c.keep_v = (l0 == LB ? 0xffffu : 0u) | (l1 == LB ? 0xffff0000u : 0u);
+    c.keep_1 = (l0 == LB - 1 ? 0xffffu : 0u) | (l1 == LB - 1 ? 0xffff0000u : 0u);
     return c;
 }
 
@@ -185,6 +190,13 @@ __device__ __forceinline__ void nwap_close_chunk(nwap_lane_stats &ls, const nwap
     }
 }
 
+// mixmode 1/2: pick the final cell of each half among the last three columns (bitwise selects)
+__device__ __forceinline__ uint32_t nwap_merge3(uint32_t v, uint32_t vm1, uint32_t vm2, const nwap_lane_cols &c)
+{
+    const uint32_t t = (vm1 & c.keep_1) | (vm2 & ~c.keep_1);
+    return (v & c.keep_v) | (t & ~c.keep_v);
+}
+
 struct nwap_true { __device__ constexpr operator bool() const { return true; } };
 struct nwap_false { __device__ constexpr operator bool() const { return false; } };
 
@@ -192,7 +204,6 @@ struct nwap_false { __device__ constexpr operator bool() const { return false; }
 // final cells for words of length LB (v) and LB-1 (vm1) -- all a sorted chunk normally
 // contains; `deep` (a chunk spanning three or more lengths: the long and short tails of a
 // strip) selects per lane among all columns.
-__device__ __forceinline__ void nwap_dp_word_any(const nwap_sym2 *, const nwap_ov_row *) {}
 template <int LB, int FLAVOR>
 __device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym2 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
                                                  const nwap_scheme_consts &sc, const nwap_ov_row *)
@@ -209,12 +220,13 @@ __device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym4 *sym, int la, c
 template <int LB, int FLAVOR, class SYM>
 __device__ __forceinline__ void nwap_row_dp(const SYM *sym, const nwap_ov_row *ovtab, int la, const uint32_t *nb,
                                             int l0, int l1, const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1,
-                                            bool deep)
+                                            uint32_t &vm2, bool deep)
 {
     uint32_t P[LB + 1];
     nwap_dp_word_sel<LB, FLAVOR>(sym, la, nb, P, sc, ovtab);
     v = P[LB];
     vm1 = P[LB >= 2 ? LB - 1 : LB];
+    vm2 = P[LB >= 3 ? LB - 2 : LB];
     if (deep) {
         uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
 #pragma unroll
@@ -230,13 +242,14 @@ __device__ __forceinline__ void nwap_row_dp(const SYM *sym, const nwap_ov_row *o
 template <int LB, int FLAVOR>
 __device__ __forceinline__ void nwap_row_dp2(const nwap_sym2 *sym, int la, const uint32_t *nbA, const uint32_t *nbB,
                                              const nwap_lane_cols &cA, const nwap_lane_cols &cB,
-                                             const nwap_scheme_consts &sc, uint32_t &vA, uint32_t &vAm1,
-                                             uint32_t &vB, uint32_t &vBm1, bool deep)
+                                             const nwap_scheme_consts &sc, uint32_t &vA, uint32_t &vAm1, uint32_t &vAm2,
+                                             uint32_t &vB, uint32_t &vBm1, uint32_t &vBm2, bool deep)
 {
     uint32_t PA[LB + 1], PB[LB + 1];
     nwap_dp_word2<LB, FLAVOR>(sym, la, nbA, nbB, PA, PB, sc);
     vA = PA[LB]; vB = PB[LB];
     vAm1 = PA[LB >= 2 ? LB - 1 : LB]; vBm1 = PB[LB >= 2 ? LB - 1 : LB];
+    vAm2 = PA[LB >= 3 ? LB - 2 : LB]; vBm2 = PB[LB >= 3 ? LB - 2 : LB];
     if (deep) {
         uint32_t alo = vA & 0xffffu, ahi = vA & 0xffff0000u, blo = vB & 0xffffu, bhi = vB & 0xffff0000u;
 #pragma unroll
@@ -271,7 +284,7 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
 #pragma unroll
     for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
-    const bool deep = mixmode > 1;
+    const bool deep = mixmode > 2;
     const int l0 = c.l0, l1 = c.l1;
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
@@ -279,14 +292,14 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
         const int la = m.la;
         if (la == 0) continue;                       // uniform across the CTA
         const typename SM::sym_t *sym = sm.rowsym[rr];
-        uint32_t v = 0, vm1 = 0;
+        uint32_t v = 0, vm1 = 0, vm2 = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
-        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, sm.ov, la, nb, l0, l1, sc, v, vm1, deep); \
+        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, sm.ov, la, nb, l0, l1, sc, v, vm1, vm2, deep); \
         break;
         switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
-        if (mixmode == 1) v = (v & c.keep_v) | (vm1 & ~c.keep_v);
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
         nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
     }
     nwap_close_chunk(ls, ca);
@@ -302,15 +315,15 @@ __device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_cons
                                                   const nwap_lane_cols &c, int mixmode, bool fast, int want_hist,
                                                   nwap_lane_stats &ls, nwap_chunk_acc &ca)
 {
-    const bool deep = mixmode > 1;
+    const bool deep = mixmode > 2;
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
         if (la == 0) continue;
-        uint32_t v, vm1;
-        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, deep);
-        if (mixmode == 1) v = (v & c.keep_v) | (vm1 & ~c.keep_v);
+        uint32_t v, vm1, vm2;
+        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
         nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
     }
 }
@@ -388,8 +401,8 @@ __device__ __forceinline__ void nwap_chunk_stream(SM &sm, const nwap_scheme_cons
         // ---- boundary: the word of band row rr is finished; x.a2 is its packed row potential ----
         uint32_t v = P[LB];
         if (mixmode) {
-            if (mixmode == 1) {
-                v = (v & c.keep_v) | (P[LB >= 2 ? LB - 1 : LB] & ~c.keep_v);
+            if (mixmode <= 2) {
+                v = nwap_merge3(v, P[LB >= 2 ? LB - 1 : LB], P[LB >= 3 ? LB - 2 : LB], c);
             } else {
                 uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
 #pragma unroll
@@ -464,23 +477,23 @@ __device__ __forceinline__ void nwap_run_chunk2(int LB, SM &sm, const nwap_schem
         nbB[j] = nwap_pack_negb(nwap_byte_of(wb0, j), nwap_byte_of(wb1, j));
     }
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
-    const bool deep = mixmode > 1;
+    const bool deep = mixmode > 2;
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
         if (la == 0) continue;
         const nwap_sym2 *sym = reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]);   // dual chains: non-override builds only
-        uint32_t vA = 0, vAm1 = 0, vB = 0, vBm1 = 0;
+        uint32_t vA = 0, vAm1 = 0, vAm2 = 0, vB = 0, vBm1 = 0, vBm2 = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
-        if (n <= DQ) nwap_row_dp2<(n <= DQ ? n : 1), FLAVOR>(sym, la, nbA, nbB, cA, cB, sc, vA, vAm1, vB, vBm1, deep); \
+        if (n <= DQ) nwap_row_dp2<(n <= DQ ? n : 1), FLAVOR>(sym, la, nbA, nbB, cA, cB, sc, vA, vAm1, vAm2, vB, vBm1, vBm2, deep); \
         break;
         switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
-        if (mixmode == 1) {
-            vA = (vA & cA.keep_v) | (vAm1 & ~cA.keep_v);
-            vB = (vB & cB.keep_v) | (vBm1 & ~cB.keep_v);
+        if (mixmode == 1 || mixmode == 2) {
+            vA = nwap_merge3(vA, vAm1, vAm2, cA);
+            vB = nwap_merge3(vB, vBm1, vBm2, cB);
         }
         nwap_emit(sm, m, m.ala2, m.rowadj, vA, cA, fast, want_hist, ls, ca);
         nwap_emit(sm, m, m.ala2, m.rowadj, vB, cB, fast, want_hist, ls, ca);
@@ -662,7 +675,9 @@ k_score_tiles(const nwap_tile_params p)
                 const int kc = item < nlc ? item * NWAP_CHUNK : nlc * NWAP_CHUNK + (item - nlc) * 2 * NWAP_CHUNK;
                 if (kc >= ncols) break;
                 const bool dual = item >= nlc && (ncols - kc) > NWAP_CHUNK;
-                const int LB = sm.clen[kc];
+                // register width of the chunk: its longest word, optionally rounded up to a multiple of
+                // NWAP_LBSTEP (fewer distinct length bodies in flight; the 3-level merge covers the slack)
+                const int LB = min(((int)sm.clen[kc] + NWAP_LBSTEP - 1) / NWAP_LBSTEP * NWAP_LBSTEP, QMAX);
                 const int ka = kc + 2 * lane, kb = ka + 1;
                 const bool va = ka < ncols, vb = kb < ncols;
                 const int la_ = va ? (int)sm.clen[ka] : LB, lb_ = vb ? (int)sm.clen[kb] : LB;
@@ -681,9 +696,8 @@ k_score_tiles(const nwap_tile_params p)
                 }
                 const nwap_lane_cols cA = nwap_make_lane_cols(off0, off1, la_, lb_, LB, sc);
                 if (OV || !dual) {
-                    const int lmin = min(la_, lb_);
-                    const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
-                                      : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
+                    const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
+                    const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
 #if NWAP_STREAM
                     if (band_simple) {
                         nwap_lane_cols cS = cA;                // dummy lanes: any in-range offset (stores are predicated off)
@@ -717,9 +731,8 @@ k_score_tiles(const nwap_tile_params p)
                         w3[4 * v] = y.x; w3[4 * v + 1] = y.y; w3[4 * v + 2] = y.z; w3[4 * v + 3] = y.w;
                     }
                     const nwap_lane_cols cB = nwap_make_lane_cols(off2, off3, ld_, le_, LB, sc);
-                    const int lmin = min(min(la_, lb_), min(ld_, le_));
-                    const int mixmode = __any_sync(0xffffffffu, lmin < LB - 1) ? 2
-                                      : __any_sync(0xffffffffu, lmin < LB) ? 1 : 0;
+                    const int lmin = __reduce_min_sync(0xffffffffu, min(min(la_, lb_), min(ld_, le_)));
+                    const int mixmode = min(LB - lmin, 3);
                     const bool fast = band_simple && (kc + 2 * NWAP_CHUNK <= ncols);
                     nwap_run_chunk2<FLAVOR, QW>(LB, sm, sc, w0, w1, w2, w3, cA, cB, mixmode, fast, p.want_hist, ls);
                 }
