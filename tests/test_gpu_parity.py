@@ -395,6 +395,41 @@ def test_full_scale_600k_two_kernels_agree(cfg, golden_samples):
             assert a == b and np.array_equal(ha, hb), (cfg, s)
 
 
+def test_c3_size_independent_properties():
+    """configs[2] at full size, properties that need no oracle:
+    (1) symmetry -- reversing the word ORDER maps edge (r, c) to (n-1-c, n-1-r) with the two words swapped,
+        and nw_score(a, b) == nw_score(b, a) (reference tests/test_aligner.py:161-170), so the two payloads
+        are related by an index permutation;
+    (2) bounds -- gap*(la+lb) <= score <= match*min(la, lb) for gap <= min(mismatch, 0)
+        (reference tests/test_aligner.py:172-184)."""
+    ids, lens, sch = synth.config_store("C3")
+    n = len(lens)
+    m, x, g = sch
+    with NwapContext(ids, lens, nw.ScoringScheme(*sch)) as fwd, \
+            NwapContext(ids[::-1].copy(), lens[::-1].copy(), nw.ScoringScheme(*sch)) as rev:
+        P = fwd.num_edges
+        a = torch.empty(P, dtype=torch.int8, device="cuda")
+        b = torch.empty(P, dtype=torch.int8, device="cuda")
+        sa = fwd.score_range(0, P, a)
+        sb = rev.score_range(0, P, b)
+        assert sa[:4] == sb[:4]                         # same multiset of scores
+        lens_t = torch.as_tensor(lens.astype(np.int64), device="cuda")
+        gen = torch.Generator(device="cuda").manual_seed(7)
+        for _ in range(4):
+            idx = torch.randint(0, P, (20_000_000,), generator=gen, device="cuda", dtype=torch.int64)
+            rows = torch.empty_like(idx)
+            cols = torch.empty_like(idx)
+            _native.check(_native.lib().nwap_rows_cols(n, idx.data_ptr(), idx.numel(), rows.data_ptr(), cols.data_ptr(),
+                                                       torch.cuda.current_stream().cuda_stream))
+            r2, c2 = n - 1 - cols, n - 1 - rows
+            idx2 = r2 * (2 * n - r2 - 1) // 2 + (c2 - r2 - 1)
+            sc = a[idx].to(torch.int64)
+            assert torch.equal(a[idx], b[idx2])
+            la, lb = lens_t[rows], lens_t[cols]
+            assert bool((sc <= m * torch.minimum(la, lb)).all()) and bool((sc >= g * (la + lb)).all())
+        del a, b
+
+
 # ---- new surface: compaction, degree, index recovery ----------------------------------------
 
 def test_compaction_and_degree(golden_cases):
