@@ -409,7 +409,7 @@ int nwap_score_range_host(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_h
         const int64_t e = std::min(end, pos + slab);
         if (k >= 2) CK(cudaStreamWaitEvent(c->s_compute, c->ev_free[b], 0));
         rc = enqueue_score(c, pos, e, c->d_slab[b], want_hist, variant, c->s_compute);
-        if (rc) return rc;
+        if (rc) { cudaStreamSynchronize(c->s_compute); cudaStreamSynchronize(c->s_copy); return rc; }
         CK(cudaEventRecord(c->ev_done[b], c->s_compute));
         CK(cudaStreamWaitEvent(c->s_copy, c->ev_done[b], 0));
         CK(cudaMemcpyAsync(out_host + (pos - start), c->d_slab[b], (size_t)(e - pos), cudaMemcpyDeviceToHost, c->s_copy));

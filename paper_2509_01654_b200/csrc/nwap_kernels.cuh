@@ -632,8 +632,10 @@ k_score_tiles(const nwap_tile_params p)
                     }
                 }
                 sm.meta[tid] = m;
-                // boundary record of the symbol stream (read only on the STREAM path)
-                nwap_stage_boundary(sm.rowsym[tid][m.la], m.ala2);
+#if NWAP_STREAM
+                // boundary record of the symbol stream; slot [la] is never written by the symbol staging below
+                if (m.la > 0) nwap_stage_boundary(sm.rowsym[tid][m.la], m.ala2);
+#endif
             }
             // stage row symbols, packed a*65537, with the row boundary values (4 symbols per item)
             for (int item = tid; item < NWAP_R * (NWAP_MAXLEN_FAST / 4); item += NWAP_THREADS) {
