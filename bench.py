@@ -363,11 +363,23 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
         assert r[3] == shard_pairs
+        # plain pinned device->host copy on this box, for context: e2e is bounded by it (5 GB per step)
+        probe_bytes = int(min(shard_pairs, 1 << 30))
+        dsrc = torch.empty(probe_bytes, dtype=torch.int8, device="cuda")
+        host[:probe_bytes].copy_(dsrc)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        host[:probe_bytes].copy_(dsrc)
+        torch.cuda.synchronize()
+        d2h_gbs = probe_bytes / (time.perf_counter() - t1) / 1e9
+        del dsrc
         qpad = ((int(lens.max()) + 15) // 16) * 16
         e2e = {"value": cells_total / (dt / args.steps) / 1e9, "unit": UNIT,
                "pairs_per_s": P / (dt / args.steps), "ms_per_step": 1e3 * dt / args.steps,
                "h2d_bytes_per_step": int(n * qpad + n), "d2h_bytes_per_step": int(shard_pairs + 2080),
-               "what": "NwapContext(host word store) + nwap_score_range_host into pinned host memory"}
+               "what": "NwapContext(host word store) + nwap_score_range_host into pinned host memory",
+               "d2h_gbs_plain_copy": d2h_gbs,
+               "d2h_bound_ms": 1e3 * shard_pairs / (d2h_gbs * 1e9)}
 
     if rank != 0:
         if world > 1:
