@@ -197,7 +197,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--words", type=int, default=0, help="override vocabulary size (default 100000*sqrt(gpus))")
-    ap.add_argument("--variant", default="auto", choices=["auto", "packed", "packed3", "simple"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "packed", "packed3", "packed_sym", "simple"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the CPU baseline sample")
     ap.add_argument("--fixed-len", type=int, default=0, help="diagnostic: all words of this length")
     ap.add_argument("--no-e2e", action="store_true")
@@ -311,15 +311,19 @@ def main():
     roof = None
     if rank == 0:
         kern_ms = float(np.mean(step_ms))                 # one k_score_tiles launch per step (+1 tiny init)
-        # the packed cell's exact instruction mix (2 DPX + 1 IMAD + 1 IADD for the default variant)
-        mix_name = "mix_2alu_2imad" if args.variant == "packed" else "cell_2dpx_imad_iadd"
+        # the packed cell's exact instruction mix (auto resolves to packed3 for a uniform scheme)
+        mix_name, instr_per_cell, mix_desc = {
+            "packed": ("mix_2alu_2imad", 4, "2 DPX + 2 IMAD"),
+            "packed_sym": ("cell_2dpx_iadd3", 3, "2 DPX + IADD3"),
+        }.get(args.variant, ("cell_2dpx_imad_iadd", 4, "2 DPX + IMAD + IADD"))
         ipc_mix, _ = probe(mix_name, 4000, local_rank)
         ipc_alu, _ = probe("vimnmx3_s16x2", 4000, local_rank)
         ipc_imad, _ = probe("imad", 4000, local_rank)
         sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
         sm_now = (clocks or {}).get("sm_mhz") or sm_max
-        # 4 warp-instructions (2 ALU + 2 IMAD) update 64 cells: cells/clk/SM = 16 * ipc
-        peak_gcups = 16.0 * ipc_mix * SM_COUNT * sm_max * 1e6 / 1e9
+        # instr_per_cell warp-instructions update one packed cell = 64 DP cells (32 lanes x s16x2)
+        cells_per_instr = 64.0 / instr_per_cell
+        peak_gcups = cells_per_instr * ipc_mix * SM_COUNT * sm_max * 1e6 / 1e9
         achieved = shard_cells / (kern_ms * 1e-3) / 1e9
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -329,11 +333,12 @@ def main():
             "traffic": traffic_from_profile(n),
             "kernel": "k_score_tiles", "kernel_ms": kern_ms,
             "algorithmic_bytes": int(shard_pairs),
-            "peak_how": (f"live probe {mix_name}: {ipc_mix:.3f} warp-instr/clk/SM on the packed cell's own 4-instruction "
-                         f"mix x 16 cells/instr x {SM_COUNT} SMs x {sm_max:.0f} MHz (clocks.max.sm); "
+            "peak_how": (f"live probe {mix_name}: {ipc_mix:.3f} warp-instr/clk/SM on the packed cell's own "
+                         f"{instr_per_cell}-instruction mix ({mix_desc}) x {cells_per_instr:.2f} cells/instr x {SM_COUNT} SMs x "
+                         f"{sm_max:.0f} MHz (clocks.max.sm); "
                          f"single-pipe probes: VIMNMX3.S16x2 {ipc_alu:.3f}, IMAD {ipc_imad:.3f} (both half-rate)"),
             "sm_mhz_under_load": sm_now,
-            "frac_at_observed_clock": achieved / (16.0 * ipc_mix * SM_COUNT * sm_now * 1e6 / 1e9),
+            "frac_at_observed_clock": achieved / (cells_per_instr * ipc_mix * SM_COUNT * sm_now * 1e6 / 1e9),
             "hbm_write": {"achieved": shard_pairs / (kern_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                           "frac": shard_pairs / (kern_ms * 1e-3) / 1e9 / hbm_peak,
                           "peak_source": "measured" if peaks else "fallback"},

@@ -44,6 +44,8 @@ extern "C" {
 #define NWAP_VARIANT_SIMPLE  1  /* one thread per pair, int32 cells, K x K table: any scheme, any q <= 255 */
 #define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 DPX + 2 IMAD per packed cell */
 #define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 2 DPX + 1 IMAD + 1 IADD per packed cell */
+#define NWAP_VARIANT_PACKED_SYM 4 /* s16x2 DPX tile kernel, symmetric gap potential: 2 DPX + 1 IADD3 per packed cell
+                                   * (needs match >= mismatch and no overrides) */
 
 typedef struct nwap_ctx nwap_ctx;
 
@@ -173,7 +175,7 @@ int nwap_rows_cols(int64_t n, const int64_t *idx_dev, int64_t count,
  * (add.u16x2, min.u16x2, fma.f16x2, max.f16x2, prmt, DPX+IADD, DPX+VIMNMX2, IMAD+IADD,
  *  IMAD+HFMA2, DPX+IMAD, alternative cell formulations, VIADDMNMX+VIMNMX3) -- names in
  * paper_2509_01654_b200/_native.py:PROBES. */
-#define NWAP_PROBE_COUNT           22
+#define NWAP_PROBE_COUNT           30
 int nwap_probe(int device, int which, int iters, double *ipc_out, double *ms_out);
 
 /* Kernels launched by this library on the calling process so far. */

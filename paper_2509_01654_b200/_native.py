@@ -16,11 +16,13 @@ LIB_PATH = Path(os.environ["NWAP_LIB"]).resolve() if os.environ.get("NWAP_LIB") 
 
 NWAP_OK, NWAP_EINVAL, NWAP_ERANGE, NWAP_ECUDA, NWAP_ENOMEM, NWAP_ECAPACITY = 0, -1, -2, -3, -4, -5
 VARIANT_AUTO, VARIANT_SIMPLE, VARIANT_PACKED, VARIANT_PACKED3 = 0, 1, 2, 3
-VARIANTS = {"auto": 0, "simple": 1, "packed": 2, "packed3": 3}
+VARIANTS = {"auto": 0, "simple": 1, "packed": 2, "packed3": 3, "packed_sym": 4}
 PROBES = ["viaddmnmx_u16x2", "vimnmx3_s16x2", "vimnmx_s16x2", "imad", "lop3", "iadd3",
           "mix_2alu_2imad", "mix_3alu_1imad", "viadd_16x2", "vimnmx_u16x2_min", "hfma2", "hmnmx2", "prmt",
           "pair_dpx_iadd", "pair_dpx_vimnmx2", "pair_imad_iadd", "pair_imad_hfma2", "pair_dpx_imad",
-          "cell_2dpx_imad_iadd", "cell_dpx_2imad_2vimnmx2", "cell_xor_min_imad_dpx_imad", "pair_viaddmnmx_vimnmx3"]
+          "cell_2dpx_imad_iadd", "cell_dpx_2imad_2vimnmx2", "cell_xor_min_imad_dpx_imad", "pair_viaddmnmx_vimnmx3",
+          "cell_2dpx_iadd3", "add_pair_dependent", "hset2_bf", "pair_hset2_dpx", "pair_add_dpx",
+          "cell_hset2_hfma2_dpx_add", "pair_hset2_imad", "pair_add_imad"]
 
 # every symbol include/nwap.h declares (tests/test_abi.py checks the two lists agree)
 EXPORTS = [

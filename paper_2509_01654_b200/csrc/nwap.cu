@@ -72,7 +72,7 @@ struct nwap_ctx {
     int64_t slab_bytes = 0;
     cudaStream_t s_compute = nullptr, s_copy = nullptr;
     cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
-    int occ_tiles[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor | ov=2, qclass) instantiation
+    int occ_tiles[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor | ov=3, qclass) instantiation
 };
 
 namespace {
@@ -84,6 +84,7 @@ tile_kernel_t tile_kernel(int flavor, int qclass, bool ov)
 {
     if (ov) return qclass == 0 ? k_score_tiles<1, 16, true> : qclass == 1 ? k_score_tiles<1, 24, true> : k_score_tiles<1, 32, true>;
     if (flavor == 0) return qclass == 0 ? k_score_tiles<0, 16, false> : qclass == 1 ? k_score_tiles<0, 24, false> : k_score_tiles<0, 32, false>;
+    if (flavor == 2) return qclass == 0 ? k_score_tiles<2, 16, false> : qclass == 1 ? k_score_tiles<2, 24, false> : k_score_tiles<2, 32, false>;
     return qclass == 0 ? k_score_tiles<1, 16, false> : qclass == 1 ? k_score_tiles<1, 24, false> : k_score_tiles<1, 32, false>;
 }
 size_t tile_smem(bool ov) { return ov ? sizeof(nwap_tile_smem_t<true>) : sizeof(nwap_tile_smem_t<false>); }
@@ -118,8 +119,13 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
 {
     if (start >= end) return NWAP_OK;
     const bool fast_ok = (!c->general || c->sparse_ov) && c->qmax <= NWAP_MAXLEN_FAST;
-    // PACKED3 (2 DPX + IMAD + IADD) measured ~8 % faster than PACKED (2 DPX + 2 IMAD): profiles/r01_ab.txt
+    const bool sym_ok = fast_ok && !c->general && nwap_flavor2_ok(c->match, c->mismatch);
+    // PACKED3 (2 DPX + IMAD + IADD) is ~8 % faster than PACKED (2 DPX + 2 IMAD) and ~14 % faster than PACKED_SYM
+    // (2 DPX + IADD3: one issue fewer, but IADD3 shares the DPX pipe): profiles/r01f_ab_packed_sym.txt
     if (variant == NWAP_VARIANT_AUTO) variant = fast_ok ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
+    if (variant == NWAP_VARIANT_PACKED_SYM && !sym_ok)
+        return fail(NWAP_EINVAL, "packed_sym kernel needs a uniform scheme with match >= mismatch and max word length <= %d (have %d%s)",
+                    NWAP_MAXLEN_FAST, c->qmax, c->general ? ", similarity overrides" : "");
     if ((variant == NWAP_VARIANT_PACKED || variant == NWAP_VARIANT_PACKED3) && !fast_ok)
         return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme (or at most %d overrides per symbol) and max word length <= %d (have %d%s)",
                     NWAP_MAX_OV, NWAP_MAXLEN_FAST, c->qmax, c->general ? ", dense similarity table" : "");
@@ -141,7 +147,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     }
 
     const bool ov = c->general;                       // here: general implies sparse_ov
-    const int flavor = (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
+    const int flavor = variant == NWAP_VARIANT_PACKED_SYM ? 2 : (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
     const int qclass = c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
     nwap_tile_params p;
     p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad;
@@ -151,12 +157,12 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.r_last = nwap_row_of(end - 1, c->n);
     p.c_end = nwap_col_of(end - 1, c->n, p.r_last);
     p.out = out_dev;
-    p.sc = nwap_make_consts(c->match, c->mismatch, c->gap);
+    p.sc = nwap_make_consts(c->match, c->mismatch, c->gap, flavor);
     p.stats = c->d_stats; p.want_hist = want_hist;
     p.unit_counter = c->d_counter;
     p.ov_table = ov ? c->d_ov : nullptr; p.ov_K = ov ? c->K : 0;
 
-    const int occ = std::max(1, c->occ_tiles[(ov ? 2 : flavor) * 3 + qclass]);
+    const int occ = std::max(1, c->occ_tiles[(ov ? 3 : flavor) * 3 + qclass]);
     const int64_t slots = (int64_t)c->sm_count * occ;
     // bands per group: as large as possible (amortises the per-unit sort) while
     // leaving >= 24 units per resident CTA for dynamic balance.
@@ -265,10 +271,10 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
         rc = build_sim_table(c, sim.data());
     }
     if (rc == NWAP_OK) {
-        for (int f = 0; f < 3 && rc == NWAP_OK; ++f)          // f == 2: sparse-override build
+        for (int f = 0; f < 4 && rc == NWAP_OK; ++f)          // f == 3: sparse-override build
             for (int w = 0; w < 3 && rc == NWAP_OK; ++w) {
-                tile_kernel_t k = tile_kernel(f == 2 ? 1 : f, w, f == 2);
-                const size_t smem = tile_smem(f == 2);
+                tile_kernel_t k = tile_kernel(f == 3 ? 1 : f, w, f == 3);
+                const size_t smem = tile_smem(f == 3);
                 guard(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cudaFuncSetAttribute");
                 int occ = 0;
                 guard(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem), "occupancy query");
@@ -578,8 +584,9 @@ int nwap_probe(int device, int which, int iters, double *ipc_out, double *ms_out
     static const probe_t table[NWAP_PROBE_COUNT] = {
         k_probe<0>, k_probe<1>, k_probe<2>, k_probe<3>, k_probe<4>, k_probe<5>, k_probe<6>, k_probe<7>,
         k_probe<8>, k_probe<9>, k_probe<10>, k_probe<11>, k_probe<12>, k_probe<13>, k_probe<14>, k_probe<15>,
-        k_probe<16>, k_probe<17>, k_probe<18>, k_probe<19>, k_probe<20>, k_probe<21>};
-    static const double per_step[NWAP_PROBE_COUNT] = {1, 1, 1, 1, 1, 1, 4, 4, 1, 1, 1, 1, 1, 2, 2, 2, 2, 2, 4, 5, 5, 2};
+        k_probe<16>, k_probe<17>, k_probe<18>, k_probe<19>, k_probe<20>, k_probe<21>, k_probe<22>, k_probe<23>,
+        k_probe<24>, k_probe<25>, k_probe<26>, k_probe<27>, k_probe<28>, k_probe<29>};
+    static const double per_step[NWAP_PROBE_COUNT] = {1, 1, 2, 1, 1, 1, 4, 4, 1, 2, 1, 2, 1, 2, 2, 2, 2, 2, 4, 5, 5, 2, 3, 2, 1, 2, 2, 4, 2, 2};
     for (int rep = 0; rep < 2; ++rep) {   // first launch warms up
         CK(cudaEventRecord(e0));
         table[which]<<<blocks, 512>>>(iters, 0x00030005u, 0xfffefffdu, 0x00070009u, 1u, sink, cycles);

@@ -21,6 +21,18 @@
 // are half-rate on separate pipes while IADD is full-rate and co-issues with both
 // (profiles/r01b_probes.txt).
 //
+// FLAVOR 2 (needs match >= mismatch) removes two of the four issues.  With the symmetric
+// potential H'[i][j] = H[i][j] - gap*(i + j) + BIAS both gap moves cost nothing and every
+// boundary cell is BIAS:
+//     H'[i][j] = max(H'[i-1][j-1] + C - out,  H'[i-1][j],  H'[i][j-1]),
+//     C = match - 2*gap,  out = D * [a_i != b_j],  D = match - mismatch >= 0.
+// Symbols are stored multiplied by 256, so (256*a - 256*b) mod 2^16 is 0 when they are equal
+// and >= 256 >= D otherwise, and ONE unsigned add-min against the threshold D yields `out`:
+//     out = VIADDMNMX.U16x2 (256*a + (-256*b), min D)     ALU pipe (half rate)
+//     dw  = IADD3           (diag - out + C*65537)         full rate, co-issues
+//     cur = VIMNMX3.S16x2   (dw, up, left)                 ALU pipe (half rate)
+// i.e. 3 issues per 2 DP cells, 2 of them on the DPX pipe, which is then the only bound.
+//
 // All halves stay inside [0, 2^15): |H| <= 128 by the int8 preflight
 // (engine.py:72-96), |(match-gap)*i| <= 192, |gap*j| <= 64, |D| <= 256, and
 // BIAS = 8192, so 32-bit IMAD never carries between halves and signed/unsigned
@@ -37,11 +49,17 @@ struct nwap_scheme_consts {
     uint32_t u2;          // (uint32)((2*gap - match) * 65537)        32-bit packed addend
     uint32_t u2h;         // uint16(2*gap - match) replicated         per-half addend (VIADDMNMX)
     uint32_t one;         // 1, opaque to the compiler so `cur*one+u2` stays an IMAD
-    int32_t alpha;        // match - gap   (row potential)
-    int32_t beta;         // gap           (column potential)
+    int32_t alpha;        // row potential per symbol:    match - gap (FLAVOR 0/1), gap (FLAVOR 2)
+    int32_t beta;         // column potential per symbol: gap
+    uint32_t symmul;      // staged row symbol = a * symmul:  65537 (FLAVOR 0/1), 256*65537 (FLAVOR 2)
+    uint32_t t2;          // FLAVOR 2: D * 65537, the add-min threshold
+    uint32_t c2;          // FLAVOR 2: (match - 2*gap) * 65537
 };
 
-NWAP_HD nwap_scheme_consts nwap_make_consts(int match, int mismatch, int gap)
+// FLAVOR 2 handles match >= mismatch only (D is an unsigned threshold there).
+NWAP_HD bool nwap_flavor2_ok(int match, int mismatch) { return match >= mismatch && match - mismatch <= 256; }
+
+NWAP_HD nwap_scheme_consts nwap_make_consts(int match, int mismatch, int gap, int flavor = 1)
 {
     nwap_scheme_consts c;
     int u = 2 * gap - match;
@@ -51,6 +69,17 @@ NWAP_HD nwap_scheme_consts nwap_make_consts(int match, int mismatch, int gap)
     c.one = 1u;
     c.alpha = match - gap;
     c.beta = gap;
+    c.symmul = 65537u;
+    c.t2 = 0u;
+    c.c2 = 0u;
+    if (flavor == 2) {
+        c.alpha = gap;
+        c.u2 = 0u;                                  // every boundary cell H'[i][0] is BIAS
+        c.u2h = 0u;
+        c.symmul = 256u * 65537u;
+        c.t2 = (uint32_t)(match - mismatch) * 65537u;
+        c.c2 = (uint32_t)((match - 2 * gap) * 65537);
+    }
     return c;
 }
 
@@ -114,6 +143,12 @@ NWAP_HD uint32_t nwap_pack_negb(uint32_t b0, uint32_t b1)
 {
     return ((0u - b0) & 0xffffu) | ((0u - b1) << 16);
 }
+// FLAVOR 2 stores symbols times 256 (see the header comment).
+template <int FLAVOR>
+NWAP_HD uint32_t nwap_pack_negb_f(uint32_t b0, uint32_t b1)
+{
+    return FLAVOR == 2 ? nwap_pack_negb(b0 << 8, b1 << 8) : nwap_pack_negb(b0, b1);
+}
 
 // One score-matrix row (one symbol of the row word, packed as a*65537) against
 // the LB register-resident columns P[1..LB] (P[0] is unused).  d0 = H'[i-1][0],
@@ -127,6 +162,20 @@ NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
                          uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc)
 {
     uint32_t left = left0;
+    if (FLAVOR == 2) {
+        // d0 arrives with C already added (d0 = BIAS2 + c2, the same for every matrix row)
+        uint32_t dw = d0 - nwap_viaddmin_u16x2(a2, nb[0], sc.t2);
+#pragma unroll
+        for (int j = 1; j <= LB; ++j) {
+            uint32_t dw_next = 0;
+            if (j < LB) dw_next = P[j] - nwap_viaddmin_u16x2(a2, nb[j], sc.t2) + sc.c2;
+            const uint32_t cur = nwap_vimax3_s16x2(dw, P[j], left);
+            P[j] = cur;
+            left = cur;
+            dw = dw_next;
+        }
+        return;
+    }
     uint32_t dw = nwap_viaddmin_u16x2(a2, nb[0], 0x00010001u) * sc.neg_delta + d0;
 #pragma unroll
     for (int j = 1; j <= LB; ++j) {
@@ -165,6 +214,15 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
     for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;        // H'[0][j]
     uint32_t d0 = NWAP_BIAS2;                               // H'[0][0]
     const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
+    if (FLAVOR == 2) {
+        const uint32_t d0c = NWAP_BIAS2 + sc.c2;            // H'[i-1][0] + C: every boundary cell is BIAS
+#pragma unroll 1
+        do {
+            const uint32_t a2 = (s++)->a2;
+            nwap_dp_row<LB, FLAVOR>(a2, nb, P, d0c, NWAP_BIAS2, sc);
+        } while (s != e);
+        return;
+    }
 #if NWAP_PREFETCH
     nwap_sym2 x = *s;
 #pragma unroll 1
@@ -277,56 +335,6 @@ inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatc
     return true;
 }
 
-// ---- dual chain: the same row word against TWO column pairs per lane (registers PA/PB) ----
-// Halves the per-matrix-row loop overhead and the per-row dispatch for short words; the two
-// chains are independent, which also doubles the ILP of the max-chain.
-template <int LB, int FLAVOR>
-NWAP_HD void nwap_dp_row2(uint32_t a2, const uint32_t *nbA, const uint32_t *nbB,
-                          uint32_t (&PA)[LB + 1], uint32_t (&PB)[LB + 1],
-                          uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc)
-{
-    uint32_t leftA = left0, leftB = left0;
-    uint32_t dwA = nwap_viaddmin_u16x2(a2, nbA[0], 0x00010001u) * sc.neg_delta + d0;
-    uint32_t dwB = nwap_viaddmin_u16x2(a2, nbB[0], 0x00010001u) * sc.neg_delta + d0;
-#pragma unroll
-    for (int j = 1; j <= LB; ++j) {
-        uint32_t dwA_next = 0, dwB_next = 0;
-        if (j < LB) {
-            dwA_next = nwap_viaddmin_u16x2(a2, nbA[j], 0x00010001u) * sc.neg_delta + PA[j];
-            dwB_next = nwap_viaddmin_u16x2(a2, nbB[j], 0x00010001u) * sc.neg_delta + PB[j];
-        }
-        const uint32_t upuA = FLAVOR == 0 ? PA[j] * sc.one + sc.u2 : PA[j] + sc.u2;
-        const uint32_t upuB = FLAVOR == 0 ? PB[j] * sc.one + sc.u2 : PB[j] + sc.u2;
-        PA[j] = nwap_vimax3_s16x2(dwA, upuA, leftA);
-        PB[j] = nwap_vimax3_s16x2(dwB, upuB, leftB);
-        leftA = PA[j]; leftB = PB[j];
-        dwA = dwA_next; dwB = dwB_next;
-    }
-}
-
-template <int LB, int FLAVOR>
-NWAP_HD void nwap_dp_word2(const nwap_sym2 *row_sym2, int la, const uint32_t *nbA, const uint32_t *nbB,
-                           uint32_t (&PA)[LB + 1], uint32_t (&PB)[LB + 1], const nwap_scheme_consts &sc)
-{
-#pragma unroll
-    for (int j = 0; j <= LB; ++j) { PA[j] = NWAP_BIAS2; PB[j] = NWAP_BIAS2; }
-    uint32_t d0 = NWAP_BIAS2;
-    const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
-#pragma unroll 1
-    do {
-#if NWAP_SYM64
-        const nwap_sym2 x = *s++;
-        const uint32_t left0 = x.left0;
-        const uint32_t a2 = x.a2;
-#else
-        const uint32_t a2 = (s++)->a2;
-        const uint32_t left0 = d0 + sc.u2;
-#endif
-        nwap_dp_row2<LB, FLAVOR>(a2, nbA, nbB, PA, PB, d0, left0, sc);
-        d0 = left0;
-    } while (s != e);
-}
-
 // Whole pair-of-pairs DP for one row word; returns the packed H' values at
 // (la, lb0) in the low half and (la, lb1) in the high half.  Used by the host
 // emulation test; the tile kernel calls nwap_dp_word directly.
@@ -343,25 +351,6 @@ NWAP_HD uint32_t nwap_dp_pair(const nwap_sym2 *row_sym2, int la, const uint32_t 
         if (j == lb1) hi = P[j] >> 16;
     }
     return lo | (hi << 16);
-}
-
-// Dual-chain counterpart of nwap_dp_pair (host emulation test): four column words.
-template <int LB, int FLAVOR>
-NWAP_HD void nwap_dp_quad(const nwap_sym2 *row_sym2, int la, const uint32_t (&nbA)[LB], const uint32_t (&nbB)[LB],
-                          const int (&lens)[4], const nwap_scheme_consts &sc, uint32_t &outA, uint32_t &outB)
-{
-    uint32_t PA[LB + 1], PB[LB + 1];
-    nwap_dp_word2<LB, FLAVOR>(row_sym2, la, nbA, nbB, PA, PB, sc);
-    uint32_t a_lo = 0, a_hi = 0, b_lo = 0, b_hi = 0;
-#pragma unroll
-    for (int j = 1; j <= LB; ++j) {
-        if (j == lens[0]) a_lo = PA[j] & 0xffffu;
-        if (j == lens[1]) a_hi = PA[j] >> 16;
-        if (j == lens[2]) b_lo = PB[j] & 0xffffu;
-        if (j == lens[3]) b_hi = PB[j] >> 16;
-    }
-    outA = a_lo | (a_hi << 16);
-    outB = b_lo | (b_hi << 16);
 }
 
 // H'[la][lb] (one half, biased) -> true score.

@@ -21,9 +21,6 @@
 #include "nwap_core.cuh"
 #include "nwap_index.cuh"
 
-#ifndef NWAP_COLD_FAMILY
-#define NWAP_COLD_FAMILY 0
-#endif
 #ifndef NWAP_LBSTEP
 #define NWAP_LBSTEP 1
 #endif
@@ -100,7 +97,6 @@ struct nwap_tile_smem_t {
     int ncols;
     int next_chunk;
     int band_simple;      // every staged row is valid over the whole sorted column window
-    int n_long_chunks;    // leading 64-column chunks that hold words longer than NWAP_DUAL_MAX
 };
 
 typedef nwap_tile_smem_t<false> nwap_tile_smem;
@@ -238,31 +234,6 @@ __device__ __forceinline__ void nwap_row_dp(const SYM *sym, const nwap_ov_row *o
     }
 }
 
-// Dual chain: two column pairs per lane (A and B), same row word.
-template <int LB, int FLAVOR>
-__device__ __forceinline__ void nwap_row_dp2(const nwap_sym2 *sym, int la, const uint32_t *nbA, const uint32_t *nbB,
-                                             const nwap_lane_cols &cA, const nwap_lane_cols &cB,
-                                             const nwap_scheme_consts &sc, uint32_t &vA, uint32_t &vAm1, uint32_t &vAm2,
-                                             uint32_t &vB, uint32_t &vBm1, uint32_t &vBm2, bool deep)
-{
-    uint32_t PA[LB + 1], PB[LB + 1];
-    nwap_dp_word2<LB, FLAVOR>(sym, la, nbA, nbB, PA, PB, sc);
-    vA = PA[LB]; vB = PB[LB];
-    vAm1 = PA[LB >= 2 ? LB - 1 : LB]; vBm1 = PB[LB >= 2 ? LB - 1 : LB];
-    vAm2 = PA[LB >= 3 ? LB - 2 : LB]; vBm2 = PB[LB >= 3 ? LB - 2 : LB];
-    if (deep) {
-        uint32_t alo = vA & 0xffffu, ahi = vA & 0xffff0000u, blo = vB & 0xffffu, bhi = vB & 0xffff0000u;
-#pragma unroll
-        for (int j = 1; j < LB; ++j) {
-            if (j == cA.l0) alo = PA[j] & 0xffffu;
-            if (j == cA.l1) ahi = PA[j] & 0xffff0000u;
-            if (j == cB.l0) blo = PB[j] & 0xffffu;
-            if (j == cB.l1) bhi = PB[j] & 0xffff0000u;
-        }
-        vA = alo | ahi; vB = blo | bhi;
-    }
-}
-
 #define NWAP_CASES_1_32                                                                        \
     NWAP_CASE(1) NWAP_CASE(2) NWAP_CASE(3) NWAP_CASE(4) NWAP_CASE(5) NWAP_CASE(6) NWAP_CASE(7) NWAP_CASE(8)         \
     NWAP_CASE(9) NWAP_CASE(10) NWAP_CASE(11) NWAP_CASE(12) NWAP_CASE(13) NWAP_CASE(14) NWAP_CASE(15) NWAP_CASE(16)  \
@@ -282,7 +253,7 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
 {
     uint32_t nb[QMAX];
 #pragma unroll
-    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb_f<FLAVOR>(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
     const bool deep = mixmode > 2;
     const int l0 = c.l0, l1 = c.l1;
@@ -305,217 +276,18 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
     nwap_close_chunk(ls, ca);
 }
 
-// NWAP_HOIST=1 (A/B): the length dispatch is done once per chunk and each length body owns the
-// whole row loop (fast emit inlined, slow emit shared through a flag).
-#ifndef NWAP_HOIST
-#define NWAP_HOIST 0
-#endif
-template <int LB, int FLAVOR, class SM>
-__device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
-                                                  const nwap_lane_cols &c, int mixmode, bool fast, int want_hist,
-                                                  nwap_lane_stats &ls, nwap_chunk_acc &ca)
-{
-    const bool deep = mixmode > 2;
-#pragma unroll 1
-    for (int rr = 0; rr < NWAP_R; ++rr) {
-        const nwap_row_meta &m = sm.meta[rr];
-        const int la = m.la;
-        if (la == 0) continue;
-        uint32_t v, vm1, vm2;
-        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
-        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
-        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
-    }
-}
+// Tried and rejected this round (same-box A/B, evidence in profiles/r01c..r01e and git history):
+// hoisting the length dispatch out of the row loop, one symbol stream per band, dual-chain
+// chunks (4 columns per lane), a cold code family for chunks spanning >= 3 lengths.
 
-template <int FLAVOR, int QMAX, int QW, class SM>
-__device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_scheme_consts &sc,
-                                                 const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
-                                                 const nwap_lane_cols &c, int mixmode, bool fast,
-                                                 int want_hist, nwap_lane_stats &ls)
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, uint32_t symmul, uint32_t left0, const nwap_ov_row *, int)
 {
-    uint32_t nb[QMAX];
-#pragma unroll
-    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
-    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
-#define NWAP_CASE(n)                                                                                       \
-    case n:                                                                                                \
-        if (n <= QMAX) nwap_chunk_rows_h<(n <= QMAX ? n : 1), FLAVOR>(sm, sc, nb, c, mixmode, fast, want_hist, ls, ca); \
-        break;
-    switch (LB) { NWAP_CASES_1_32 default: break; }
-#undef NWAP_CASE
-    nwap_close_chunk(ls, ca);
+    x.a2 = a * symmul; x.left0 = left0;
 }
-
-// ---------------------------------------------------------------------------
-// STREAM path (NWAP_STREAM=1): the 16 row words of a simple band are one symbol stream in shared
-// memory -- rowsym[rr][0..la) are the matrix rows of word rr and rowsym[rr][la] is a BOUNDARY record
-// {alpha*la*65537, left0 = 0}.  A chunk then needs ONE length dispatch and ONE loop: at a boundary the
-// length-specialised body itself stores the two score bytes, updates the packed statistics,
-// re-initialises the rolling row and jumps to the next word.  No per-row dispatch, no per-row
-// prologue.  Lanes beyond the end of the sorted list recompute the chunk's first column; their stores
-// are predicated off (st0/st1) and their sums masked (vmask); min/max may see the duplicates.
-// ---------------------------------------------------------------------------
-// A/B-tested and REJECTED (profiles/r01e_ab_stream_hoist.txt): +9 % at L = 4 but -5..-8 % at L >= 8
-// (four extra moves + a test per matrix row) and -4 % / -19 % on the 100k / 20k French-shaped
-// workloads (a second code family next to the per-row path).  Compiled out by default.
-#ifndef NWAP_STREAM
-#define NWAP_STREAM 0
-#endif
-
-// one matrix row from a stream record, plain or sparse-override
-template <int LB, int FLAVOR>
-__device__ __forceinline__ void nwap_dp_row_any(const nwap_sym2 &x, const uint32_t *nb, uint32_t (&P)[LB + 1],
-                                                uint32_t d0, const nwap_scheme_consts &sc, const nwap_ov_row *)
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_t symmul, uint32_t left0, const nwap_ov_row *ov, int K)
 {
-    nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
-}
-template <int LB, int FLAVOR>
-__device__ __forceinline__ void nwap_dp_row_any(const nwap_sym4 &x, const uint32_t *nb, uint32_t (&P)[LB + 1],
-                                                uint32_t d0, const nwap_scheme_consts &sc, const nwap_ov_row *ovtab)
-{
-    if (x.ovi == NWAP_NO_OV) nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
-    else nwap_dp_row_ov<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc, ovtab[x.ovi]);
-}
-
-template <int LB, int FLAVOR, class SM>
-__device__ __forceinline__ void nwap_chunk_stream(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
-                                                  const nwap_lane_cols &c, int mixmode, bool st0, bool st1,
-                                                  uint32_t vmask, nwap_lane_stats &ls, uint32_t &acc, uint32_t &acc_hi)
-{
-    typedef typename SM::sym_t sym_t;
-    uint32_t P[LB + 1];
-#pragma unroll
-    for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
-    uint32_t d0 = NWAP_BIAS2;
-    int rr = 0;
-    const sym_t *s = sm.rowsym[0];
-#pragma unroll 1
-    for (;;) {
-        const sym_t x = *s++;
-        if (x.left0 != 0u) {
-            nwap_dp_row_any<LB, FLAVOR>(x, nb, P, d0, sc, sm.ov);
-            d0 = x.left0;
-            continue;
-        }
-        // ---- boundary: the word of band row rr is finished; x.a2 is its packed row potential ----
-        uint32_t v = P[LB];
-        if (mixmode) {
-            if (mixmode <= 2) {
-                v = nwap_merge3(v, P[LB >= 2 ? LB - 1 : LB], P[LB >= 3 ? LB - 2 : LB], c);
-            } else {
-                uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
-#pragma unroll
-                for (int j = 1; j < LB; ++j) {
-                    if (j == c.l0) lo = P[j] & 0xffffu;
-                    if (j == c.l1) hi = P[j] & 0xffff0000u;
-                }
-                v = lo | hi;
-            }
-        }
-        const uint32_t t = v + x.a2 + c.kpos2;       // halves: score + BIAS
-        const uint32_t thi = t >> 16;
-        const int adj = sm.meta[rr].rowadj;
-        if (st0) sm.out[adj + (int)c.off0] = (uint8_t)t;
-        if (st1) sm.out[adj + (int)c.off1] = (uint8_t)thi;
-        ls.mn2 = __vmins2(ls.mn2, t);
-        ls.mx2 = __vmaxs2(ls.mx2, t);
-        const uint32_t tm = t & vmask;
-        acc += tm;
-        acc_hi += tm >> 16;
-        if (++rr == NWAP_R) break;
-        s = sm.rowsym[rr];
-#pragma unroll
-        for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
-        d0 = NWAP_BIAS2;
-    }
-}
-
-template <int FLAVOR, int QMAX, int QW, class SM>
-__device__ __forceinline__ void nwap_run_chunk_stream(int LB, SM &sm, const nwap_scheme_consts &sc,
-                                                      const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
-                                                      const nwap_lane_cols &c, int mixmode, bool va, bool vb,
-                                                      nwap_lane_stats &ls)
-{
-    uint32_t nb[QMAX];
-#pragma unroll
-    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
-    const uint32_t vmask = (va ? 0xffffu : 0u) | (vb ? 0xffff0000u : 0u);
-    uint32_t acc = 0, acc_hi = 0;
-#define NWAP_CASE(n)                                                                                       \
-    case n:                                                                                                \
-        if (n <= QMAX) nwap_chunk_stream<(n <= QMAX ? n : 1), FLAVOR>(sm, sc, nb, c, mixmode, va, vb, vmask, ls, acc, acc_hi); \
-        break;
-    switch (LB) { NWAP_CASES_1_32 default: break; }
-#undef NWAP_CASE
-    // acc = sum(lo) + 65536 * sum(hi) (mod 2^32), acc_hi = sum(hi); all R rows of a simple band are present
-    const int nvalid = (va ? 1 : 0) + (vb ? 1 : 0);
-    const uint32_t sum_lo = acc - (acc_hi << 16);
-    ls.sum += (long long)sum_lo + (long long)acc_hi - (long long)(NWAP_R * nvalid) * (long long)NWAP_BIAS;
-    ls.count += NWAP_R * nvalid;
-}
-
-// Dual-chain chunk: 128 sorted columns (4 per lane), every word no longer than NWAP_DUAL_MAX.
-// A/B-tested and REJECTED (profiles/r01d_ab_dual.txt: 8.8 vs 10.5 TCUPS at DUAL_MAX=12): inside
-// the DP loops the kernel is already DPX-pipe-bound, so halving the loop overhead buys nothing
-// and the larger bodies cost instruction-cache hits.  Kept compiled out (0) for the record.
-#ifndef NWAP_DUAL_MAX
-#define NWAP_DUAL_MAX 0
-#endif
-template <int FLAVOR, int QW, class SM>
-__device__ __forceinline__ void nwap_run_chunk2(int LB, SM &sm, const nwap_scheme_consts &sc,
-                                                const uint32_t (&wa0)[QW], const uint32_t (&wa1)[QW],
-                                                const uint32_t (&wb0)[QW], const uint32_t (&wb1)[QW],
-                                                const nwap_lane_cols &cA, const nwap_lane_cols &cB,
-                                                int mixmode, bool fast, int want_hist, nwap_lane_stats &ls)
-{
-    constexpr int DQ = NWAP_DUAL_MAX > 0 ? NWAP_DUAL_MAX : 1;
-    uint32_t nbA[DQ], nbB[DQ];
-#pragma unroll
-    for (int j = 0; j < DQ; ++j) {
-        nbA[j] = nwap_pack_negb(nwap_byte_of(wa0, j), nwap_byte_of(wa1, j));
-        nbB[j] = nwap_pack_negb(nwap_byte_of(wb0, j), nwap_byte_of(wb1, j));
-    }
-    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
-    const bool deep = mixmode > 2;
-#pragma unroll 1
-    for (int rr = 0; rr < NWAP_R; ++rr) {
-        const nwap_row_meta &m = sm.meta[rr];
-        const int la = m.la;
-        if (la == 0) continue;
-        const nwap_sym2 *sym = reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]);   // dual chains: non-override builds only
-        uint32_t vA = 0, vAm1 = 0, vAm2 = 0, vB = 0, vBm1 = 0, vBm2 = 0;
-#define NWAP_CASE(n)                                                                                       \
-    case n:                                                                                                \
-        if (n <= DQ) nwap_row_dp2<(n <= DQ ? n : 1), FLAVOR>(sym, la, nbA, nbB, cA, cB, sc, vA, vAm1, vAm2, vB, vBm1, vBm2, deep); \
-        break;
-        switch (LB) { NWAP_CASES_1_32 default: break; }
-#undef NWAP_CASE
-        if (mixmode == 1 || mixmode == 2) {
-            vA = nwap_merge3(vA, vAm1, vAm2, cA);
-            vB = nwap_merge3(vB, vBm1, vBm2, cB);
-        }
-        nwap_emit(sm, m, m.ala2, m.rowadj, vA, cA, fast, want_hist, ls, ca);
-        nwap_emit(sm, m, m.ala2, m.rowadj, vB, cB, fast, want_hist, ls, ca);
-    }
-    // two emits per row: rows_fast counted twice, which is what nwap_close_chunk expects (2 scores each)
-    nwap_close_chunk(ls, ca);
-}
-
-__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, uint32_t left0, const nwap_ov_row *, int)
-{
-    x.a2 = a * 65537u; x.left0 = left0;
-}
-__device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_t left0, const nwap_ov_row *ov, int K)
-{
-    x.a2 = a * 65537u; x.left0 = left0; x.pad = 0;
+    x.a2 = a * symmul; x.left0 = left0; x.pad = 0;
     x.ovi = ((int)a < K && ov[a].count) ? a : NWAP_NO_OV;
-}
-
-__device__ __forceinline__ void nwap_stage_boundary(nwap_sym2 &x, uint32_t ala2) { x.a2 = ala2; x.left0 = 0u; }
-__device__ __forceinline__ void nwap_stage_boundary(nwap_sym4 &x, uint32_t ala2)
-{
-    x.a2 = ala2; x.left0 = 0u; x.ovi = NWAP_NO_OV; x.pad = 0u;
 }
 
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
@@ -587,13 +359,10 @@ k_score_tiles(const nwap_tile_params p)
         }
         __syncthreads();
         if (tid == 0) {
-            int run = 0, nlong = 0;
-            for (int len = MAXL; len >= 1; --len) {
+            int run = 0;
+            for (int len = MAXL; len >= 1; --len)
                 for (int w = 0; w < NWAP_WARPS; ++w) { int cnt = sm.bins[w][len]; sm.bins[w][len] = run; run += cnt; }
-                if (len == NWAP_DUAL_MAX + 1) nlong = run;      // columns with words longer than NWAP_DUAL_MAX
-            }
             sm.ncols = run;
-            sm.n_long_chunks = NWAP_DUAL_MAX > 0 ? (nlong + NWAP_CHUNK - 1) / NWAP_CHUNK : (run + NWAP_CHUNK - 1) / NWAP_CHUNK;
         }
         __syncthreads();
 #pragma unroll
@@ -632,10 +401,6 @@ k_score_tiles(const nwap_tile_params p)
                     }
                 }
                 sm.meta[tid] = m;
-#if NWAP_STREAM
-                // boundary record of the symbol stream; slot [la] is never written by the symbol staging below
-                if (m.la > 0) nwap_stage_boundary(sm.rowsym[tid][m.la], m.ala2);
-#endif
             }
             // stage row symbols, packed a*65537, with the row boundary values (4 symbols per item)
             for (int item = tid; item < NWAP_R * (NWAP_MAXLEN_FAST / 4); item += NWAP_THREADS) {
@@ -648,7 +413,7 @@ k_score_tiles(const nwap_tile_params p)
                     for (int e = 0; e < 4; ++e) {
                         const uint32_t a = (v >> (8 * e)) & 0xffu;
                         if (q4 * 4 + e < la_r)           // slot [la] belongs to the boundary record
-                            nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
+                            nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, sc.symmul, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
                                            sm.ov, p.ov_K);
                     }
                 }
@@ -668,15 +433,12 @@ k_score_tiles(const nwap_tile_params p)
             // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
             const int ncols = sm.ncols;
             const bool band_simple = sm.band_simple != 0;
-            const int nlc = sm.n_long_chunks;
             for (;;) {
                 int item = 0;
                 if (lane == 0) item = atomicAdd(&sm.next_chunk, 1);
                 item = __shfl_sync(0xffffffffu, item, 0);
-                // items 0..nlc-1: single 64-column chunks (long words); then 128-column dual chunks
-                const int kc = item < nlc ? item * NWAP_CHUNK : nlc * NWAP_CHUNK + (item - nlc) * 2 * NWAP_CHUNK;
+                const int kc = item * NWAP_CHUNK;
                 if (kc >= ncols) break;
-                const bool dual = item >= nlc && (ncols - kc) > NWAP_CHUNK;
                 // register width of the chunk: its longest word, optionally rounded up to a multiple of
                 // NWAP_LBSTEP (fewer distinct length bodies in flight; the 3-level merge covers the slack)
                 const int LB = min(((int)sm.clen[kc] + NWAP_LBSTEP - 1) / NWAP_LBSTEP * NWAP_LBSTEP, QMAX);
@@ -697,47 +459,10 @@ k_score_tiles(const nwap_tile_params p)
                     w1[4 * v] = y.x; w1[4 * v + 1] = y.y; w1[4 * v + 2] = y.z; w1[4 * v + 3] = y.w;
                 }
                 const nwap_lane_cols cA = nwap_make_lane_cols(off0, off1, la_, lb_, LB, sc);
-                if (OV || !dual) {
-                    const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
-                    const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
-#if NWAP_STREAM
-                    if (band_simple) {
-                        nwap_lane_cols cS = cA;                // dummy lanes: any in-range offset (stores are predicated off)
-                        if (!va) cS.off0 = 0u;
-                        if (!vb) cS.off1 = 0u;
-                        nwap_run_chunk_stream<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cS, mixmode, va, vb, ls);
-                        continue;
-                    }
-#endif
-                    const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
-#if NWAP_HOIST
-                    nwap_run_chunk_h<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
-#else
-                    nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
-#endif
-                } else {
-                    const int kc2 = kc + NWAP_CHUNK;
-                    const int kd = kc2 + 2 * lane, ke = kd + 1;
-                    const bool vd = kd < ncols, ve = ke < ncols;
-                    const int ld_ = vd ? (int)sm.clen[kd] : LB, le_ = ve ? (int)sm.clen[ke] : LB;
-                    const uint32_t off2 = vd ? (uint32_t)sm.cols[kd] : 0xffffu;
-                    const uint32_t off3 = ve ? (uint32_t)sm.cols[ke] : 0xffffu;
-                    const int64_t cd = strip_lo + (vd ? sm.cols[kd] : sm.cols[kc]);
-                    const int64_t ce = strip_lo + (ve ? sm.cols[ke] : sm.cols[kc]);
-                    uint32_t w2[QW], w3[QW];
-#pragma unroll
-                    for (int v = 0; v < QW / 4; ++v) {
-                        const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p.ids + cd * p.qpad) + v);
-                        const uint4 y = __ldg(reinterpret_cast<const uint4 *>(p.ids + ce * p.qpad) + v);
-                        w2[4 * v] = x.x; w2[4 * v + 1] = x.y; w2[4 * v + 2] = x.z; w2[4 * v + 3] = x.w;
-                        w3[4 * v] = y.x; w3[4 * v + 1] = y.y; w3[4 * v + 2] = y.z; w3[4 * v + 3] = y.w;
-                    }
-                    const nwap_lane_cols cB = nwap_make_lane_cols(off2, off3, ld_, le_, LB, sc);
-                    const int lmin = __reduce_min_sync(0xffffffffu, min(min(la_, lb_), min(ld_, le_)));
-                    const int mixmode = min(LB - lmin, 3);
-                    const bool fast = band_simple && (kc + 2 * NWAP_CHUNK <= ncols);
-                    nwap_run_chunk2<FLAVOR, QW>(LB, sm, sc, w0, w1, w2, w3, cA, cB, mixmode, fast, p.want_hist, ls);
-                }
+                const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
+                const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
+                const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
+                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
             }
             __syncthreads();
 
@@ -1165,10 +890,10 @@ k_probe(int iters, uint32_t a, uint32_t b, uint32_t c, uint32_t one, uint32_t *s
             for (int k = 0; k < 8; ++k) {
                 if (WHICH == 0) nwap_p_viaddmin(x[k], b, c);
                 else if (WHICH == 1) nwap_p_vimax3(x[k], b, y[k]);
-                else if (WHICH == 2) NWAP_OP2("max.s16x2", x[k], y[k]);
+                else if (WHICH == 2) { NWAP_OP2("max.s16x2", x[k], y[k]); NWAP_OP2("max.s16x2", y[k], x[k]); }   // dependent pair: ptxas cannot fuse it into VIMNMX3
                 else if (WHICH == 3) nwap_p_imad(x[k], a, b);
                 else if (WHICH == 4) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[k]) : "r"(b), "r"(y[k]));
-                else if (WHICH == 5) NWAP_OP2("add.u32", x[k], y[k]);
+                else if (WHICH == 5) asm volatile("{.reg .b32 t; add.u32 t, %0, %1; add.u32 %0, t, %2;}" : "+r"(x[k]) : "r"(y[k]), "r"(b));   // one IADD3
                 else if (WHICH == 6) {                                    // 2 DPX + 2 IMAD cell
                     uint32_t e = a; nwap_p_viaddmin(e, y[k], 0x00010001u);
                     nwap_p_imad(e, b, x[k]);
@@ -1181,9 +906,9 @@ k_probe(int iters, uint32_t a, uint32_t b, uint32_t c, uint32_t one, uint32_t *s
                     NWAP_OP2("max.s16x2", x[k], y[k]);
                 }
                 else if (WHICH == 8) NWAP_OP2("add.u16x2", x[k], y[k]);
-                else if (WHICH == 9) NWAP_OP2("min.u16x2", x[k], y[k]);
+                else if (WHICH == 9) { NWAP_OP2("min.u16x2", x[k], y[k]); NWAP_OP2("min.u16x2", y[k], x[k]); }
                 else if (WHICH == 10) asm volatile("fma.rn.f16x2 %0, %0, %1, %2;" : "+r"(x[k]) : "r"(a), "r"(b));
-                else if (WHICH == 11) NWAP_OP2("max.f16x2", x[k], y[k]);
+                else if (WHICH == 11) { NWAP_OP2("max.f16x2", x[k], y[k]); NWAP_OP2("max.f16x2", y[k], x[k]); }
                 else if (WHICH == 12) asm volatile("prmt.b32 %0, %0, %1, %2;" : "+r"(x[k]) : "r"(y[k]), "r"(b));
                 else if (WHICH == 13) { nwap_p_vimax3(x[k], b, c); NWAP_OP2("add.u32", y[k], a); }          // DPX + IADD
                 else if (WHICH == 14) { nwap_p_vimax3(x[k], b, c); NWAP_OP2("max.s16x2", y[k], a); }        // DPX + VIMNMX2
@@ -1206,6 +931,32 @@ k_probe(int iters, uint32_t a, uint32_t b, uint32_t c, uint32_t one, uint32_t *s
                     nwap_p_vimax3(x[k], e, y[k]);
                     y[k] = x[k]; nwap_p_imad(y[k], one, c);
                 } else if (WHICH == 21) { nwap_p_viaddmin(x[k], b, c); nwap_p_vimax3(y[k], b, c); }         // two DPX kinds
+                else if (WHICH == 23) {                                   // dependent add pair (cannot be merged)
+                    NWAP_OP2("add.u32", x[k], y[k]); NWAP_OP2("add.u32", y[k], x[k]);
+                } else if (WHICH == 24) asm volatile("set.ne.f16x2.f16x2 %0, %0, %1;" : "+r"(x[k]) : "r"(y[k]));   // HSET2.BF
+                else if (WHICH == 25) {                                   // HSET2 + DPX
+                    asm volatile("set.ne.f16x2.f16x2 %0, %0, %1;" : "+r"(x[k]) : "r"(b));
+                    nwap_p_vimax3(y[k], b, c);
+                } else if (WHICH == 26) {                                 // dependent adds + DPX, 1:1
+                    uint32_t &w = x[(k + 4) & 7];
+                    if (k < 4) { NWAP_OP2("add.u32", x[k], w); nwap_p_vimax3(y[k], b, c); NWAP_OP2("add.u32", w, x[k]); nwap_p_vimax3(y[k + 4], b, c); }
+                } else if (WHICH == 27) {                                 // fp16-compare cell: HSET2 + HFMA2 + DPX + add
+                    uint32_t e = a; asm volatile("set.ne.f16x2.f16x2 %0, %0, %1;" : "+r"(e) : "r"(y[k]));
+                    asm volatile("fma.rn.f16x2 %0, %0, %1, %2;" : "+r"(e) : "r"(b), "r"(x[k]));
+                    nwap_p_vimax3(x[k], e, y[k]);
+                    y[k] = x[k]; NWAP_OP2("add.u32", y[k], c);
+                } else if (WHICH == 28) {                                 // HSET2 + IMAD
+                    asm volatile("set.ne.f16x2.f16x2 %0, %0, %1;" : "+r"(x[k]) : "r"(b));
+                    nwap_p_imad(y[k], a, b);
+                } else if (WHICH == 29) {                                 // dependent adds + IMAD, 1:1
+                    uint32_t &w = x[(k + 4) & 7];
+                    if (k < 4) { NWAP_OP2("add.u32", x[k], w); nwap_p_imad(y[k], a, b); NWAP_OP2("add.u32", w, x[k]); nwap_p_imad(y[k + 4], a, b); }
+                }
+                else if (WHICH == 22) {                                   // symmetric-potential cell: 2 DPX + IADD3
+                    uint32_t e = a; nwap_p_viaddmin(e, x[k], c);
+                    asm volatile("{.reg .b32 t; sub.u32 t, %1, %0; add.u32 %0, t, %2;}" : "+r"(e) : "r"(x[k]), "r"(b));
+                    nwap_p_vimax3(x[k], e, y[k]);
+                }
             }
         }
     }

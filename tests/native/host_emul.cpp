@@ -12,12 +12,12 @@ static uint32_t run_pair(const uint8_t *a, int la, const uint8_t *b0, int lb0,
 {
     nwap_sym2 row2[256];
     for (int i = 0; i < la; ++i) {
-        row2[i].a2 = (uint32_t)a[i] * 65537u;
+        row2[i].a2 = (uint32_t)a[i] * sc.symmul;
         row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
     }
     uint32_t nb[LB];
     for (int j = 0; j < LB; ++j)
-        nb[j] = nwap_pack_negb(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
+        nb[j] = nwap_pack_negb_f<FLAVOR>(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
     return nwap_dp_pair<LB, FLAVOR>(row2, la, nb, lb0, lb1, sc);
 }
 
@@ -34,29 +34,6 @@ static uint32_t dispatch(int LB, const uint8_t *a, int la, const uint8_t *b0, in
 #undef CASE
     }
     return 0;
-}
-
-template <int LB, int FLAVOR>
-static void run_quad(const uint8_t *a, int la, const uint8_t *const b[4], const int lb[4],
-                     const nwap_scheme_consts &sc, int *scores)
-{
-    nwap_sym2 row2[256];
-    for (int i = 0; i < la; ++i) {
-        row2[i].a2 = (uint32_t)a[i] * 65537u;
-        row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
-    }
-    uint32_t nbA[LB], nbB[LB];
-    for (int j = 0; j < LB; ++j) {
-        nbA[j] = nwap_pack_negb(j < lb[0] ? b[0][j] : 0u, j < lb[1] ? b[1][j] : 0u);
-        nbB[j] = nwap_pack_negb(j < lb[2] ? b[2][j] : 0u, j < lb[3] ? b[3][j] : 0u);
-    }
-    const int lens[4] = {lb[0], lb[1], lb[2], lb[3]};
-    uint32_t oa, ob;
-    nwap_dp_quad<LB, FLAVOR>(row2, la, nbA, nbB, lens, sc, oa, ob);
-    scores[0] = nwap_unbias(oa & 0xffffu, la, lb[0], sc);
-    scores[1] = nwap_unbias(oa >> 16, la, lb[1], sc);
-    scores[2] = nwap_unbias(ob & 0xffffu, la, lb[2], sc);
-    scores[3] = nwap_unbias(ob >> 16, la, lb[3], sc);
 }
 
 template <int LB>
@@ -106,33 +83,17 @@ int emul_pair_scores_ov(int LB, const uint8_t *a, int la, const uint8_t *b0, int
     return 0;
 }
 
-// Dual chain: (a vs b0..b3) at register width LB (<= 16 here).
-int emul_quad_scores(int flavor, int LB, const uint8_t *a, int la, const uint8_t *b0, const uint8_t *b1,
-                     const uint8_t *b2, const uint8_t *b3, const int *lb, int match, int mismatch, int gap,
-                     int *scores)
-{
-    if (LB < 1 || LB > 16 || la < 1) return -1;
-    for (int k = 0; k < 4; ++k) if (lb[k] < 1 || lb[k] > LB) return -1;
-    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap);
-    const uint8_t *const b[4] = {b0, b1, b2, b3};
-    switch (LB) {
-#define CASE(n) case n: if (flavor == 0) run_quad<n, 0>(a, la, b, lb, sc, scores); else run_quad<n, 1>(a, la, b, lb, sc, scores); return 0;
-        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-    }
-    return -1;
-}
-
 // Scores (a vs b0) and (a vs b1) with the packed recurrence at register width LB.
 int emul_pair_scores(int flavor, int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0,
                      const uint8_t *b1, int lb1, int match, int mismatch, int gap,
                      int *s0, int *s1)
 {
     if (LB < 1 || LB > 32 || lb0 > LB || lb1 > LB || la < 1 || lb0 < 1 || lb1 < 1) return -1;
-    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap);
+    if (flavor == 2 && !nwap_flavor2_ok(match, mismatch)) return -3;
+    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap, flavor);
     uint32_t v = flavor == 0 ? dispatch<0>(LB, a, la, b0, lb0, b1, lb1, sc)
-                             : dispatch<1>(LB, a, la, b0, lb0, b1, lb1, sc);
+               : flavor == 1 ? dispatch<1>(LB, a, la, b0, lb0, b1, lb1, sc)
+                             : dispatch<2>(LB, a, la, b0, lb0, b1, lb1, sc);
     *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
     *s1 = nwap_unbias(v >> 16, la, lb1, sc);
     return 0;

@@ -14,8 +14,14 @@ from conftest import GOLDEN
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-FAST = ["packed", "packed3"]
-ALL = ["packed", "packed3", "simple"]
+FAST = ["packed", "packed3", "packed_sym"]
+ALL = ["packed", "packed3", "packed_sym", "simple"]
+
+
+def _allowed(variants, scheme):
+    """packed_sym (2 DPX + IADD3 cell) needs match >= mismatch and no overrides."""
+    ok = scheme.match >= scheme.mismatch and not scheme.overrides
+    return [v for v in variants if v != "packed_sym" or ok]
 
 
 class CollectSink:
@@ -146,7 +152,7 @@ def test_golden_engine_cases(golden_cases, name):
     with NwapContext(c["ids"], c["lengths"], scheme) as ctx:
         # sparse overrides run on the packed kernel too; q > 32 only on the generic one
         variants = ["simple"] if ctx.max_len > 32 else (["packed3", "simple"] if c.get("overrides") else ALL)
-        for v in variants + ["auto"]:
+        for v in _allowed(variants, scheme) + ["auto"]:
             got, st = _score(ctx, 0, P, v, want_hist=True)
             assert np.array_equal(got, c["payload"]), (name, v)
             ssum, smin, smax, scount, hist = st
@@ -209,9 +215,12 @@ def test_random_schemes_all_variants():
         P = nw.num_edges(n)
         ref, *_ = _oracle(ids, lens, scheme, 0, P)
         with NwapContext(ids, lens, scheme) as ctx:
-            for v in ALL:
+            for v in _allowed(ALL, scheme) + ["auto"]:
                 got, _ = _score(ctx, 0, P, v)
                 assert np.array_equal(got, ref), (trial, v, (m, x, g), q)
+            if m < x:
+                with pytest.raises(ValueError, match="packed_sym"):
+                    ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed_sym")
 
 
 def test_sparse_override_schemes_on_the_packed_kernel():

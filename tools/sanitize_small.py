@@ -17,7 +17,7 @@ P = nw.num_edges(n)
 sim = orc.similarity_matrix(1, -1, int(ids.max()) + 1)
 ref, rsum, rmin, rmax = orc.c_score_range(ids.astype(np.int32), lens.astype(np.int32), sim, -2, n, 0, P, threads=4)
 with NwapContext(ids, lens, nw.ScoringScheme(1, -1, -2)) as ctx:
-    for variant in ("packed", "packed3", "simple"):
+    for variant in ("packed", "packed3", "packed_sym", "simple"):
         out = torch.empty(P + 3, dtype=torch.int8, device="cuda")[3:]
         st = ctx.score_range(5, P - 7, out, want_hist=True, variant=variant)
         got = out[: P - 12].cpu().numpy()
