@@ -92,6 +92,12 @@ int nwap_set_similarity(nwap_ctx *ctx, const int8_t *sim, int K);
 
 void nwap_destroy(nwap_ctx *ctx);
 
+/* nwap_destroy returns the context's host-destination pipeline (two device slabs, two streams,
+ * four events) and its small device arrays to a per-device cache, so the create -> score ->
+ * destroy cycle of the reference-shaped entry point costs no driver allocation after the first
+ * call.  nwap_trim() frees everything cached, on every device. */
+void nwap_trim(void);
+
 int64_t nwap_num_words(const nwap_ctx *ctx);
 int64_t nwap_num_edges(const nwap_ctx *ctx);   /* triangle.py:36-40 */
 int     nwap_max_len(const nwap_ctx *ctx);
@@ -112,6 +118,14 @@ int nwap_score_range(nwap_ctx *ctx, int64_t start, int64_t end, int8_t *out_dev,
  * end-to-end number is measured through. */
 int nwap_score_range_host(nwap_ctx *ctx, int64_t start, int64_t end, int8_t *out_host,
                           nwap_stats *stats_host, int want_hist, int variant);
+
+/* The same call split in two, so a caller can consume slab k (sink.write, engine.py:256) while
+ * the device scores and copies slab k+1 into another host buffer: _begin enqueues the whole
+ * range and returns immediately; _wait blocks until out_host is complete and returns the
+ * statistics.  One call in flight per context; out_host must stay valid until _wait. */
+int nwap_score_range_host_begin(nwap_ctx *ctx, int64_t start, int64_t end, int8_t *out_host,
+                                int want_hist, int variant);
+int nwap_score_range_host_wait(nwap_ctx *ctx, nwap_stats *stats_host);
 
 /* Statistics of the most recent asynchronous nwap_score_range on `stream`. */
 int nwap_read_stats(nwap_ctx *ctx, nwap_stats *stats_host, void *stream);

@@ -28,7 +28,8 @@ PROBES = ["viaddmnmx_u16x2", "vimnmx3_s16x2", "vimnmx_s16x2", "imad", "lop3", "i
 EXPORTS = [
     "nwap_version", "nwap_last_error", "nwap_device_count", "nwap_preflight", "nwap_create",
     "nwap_set_similarity", "nwap_destroy", "nwap_num_words", "nwap_num_edges", "nwap_max_len",
-    "nwap_cells_in_range", "nwap_score_range", "nwap_score_range_host", "nwap_read_stats",
+    "nwap_cells_in_range", "nwap_score_range", "nwap_score_range_host", "nwap_score_range_host_begin",
+    "nwap_score_range_host_wait", "nwap_trim", "nwap_read_stats",
     "nwap_payload_stats", "nwap_compact_range", "nwap_filter_normalized", "nwap_hist_normalized",
     "nwap_equal_work_bounds", "nwap_rows_cols",
     "nwap_probe", "nwap_launch_count",
@@ -83,6 +84,9 @@ def lib() -> ctypes.CDLL:
         "nwap_cells_in_range": (i64, [p, i64, i64]),
         "nwap_score_range": (i32, [p, i64, i64, p, p, i32, i32, p]),
         "nwap_score_range_host": (i32, [p, i64, i64, p, p, i32, i32]),
+        "nwap_score_range_host_begin": (i32, [p, i64, i64, p, i32, i32]),
+        "nwap_score_range_host_wait": (i32, [p, p]),
+        "nwap_trim": (None, []),
         "nwap_read_stats": (i32, [p, p, p]),
         "nwap_payload_stats": (i32, [p, p, i64, p, p]),
         "nwap_compact_range": (i32, [p, p, i64, i64, i32, p, p, i64, p, p, p]),

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -67,17 +68,50 @@ struct nwap_ctx {
     long long *d_block_counts = nullptr;
     int64_t block_counts_cap = 0;
     long long *d_total = nullptr;
-    // host-destination pipeline
+    // host-destination pipeline: borrowed from the per-device cache on first use, returned in nwap_destroy
+    struct nwap_pipe *pipe = nullptr;
+    bool host_pending = false;          // nwap_score_range_host_begin issued, nwap_score_range_host_wait not yet
+    int occ_tiles[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor | ov=3, qclass) instantiation
+};
+
+// Two device slabs, two streams and four events: everything nwap_score_range_host needs to overlap
+// scoring with the device->host copies.
+struct nwap_pipe {
     int8_t *d_slab[2] = {nullptr, nullptr};
     int64_t slab_bytes = 0;
     cudaStream_t s_compute = nullptr, s_copy = nullptr;
     cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
-    int occ_tiles[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor | ov=3, qclass) instantiation
 };
 
 namespace {
 
 typedef void (*tile_kernel_t)(const nwap_tile_params);
+
+// Per-device facts and scratch that outlive a context.  Creating and destroying a context per
+// call (what the reference-shaped entry point does) must not pay cudaGetDeviceProperties, twelve
+// occupancy queries, two 256 MB cudaMalloc/cudaFree pairs and stream/event creation every time:
+// those were 60 % of the end-to-end step.  nwap_trim() releases the cached scratch.
+struct device_cache {
+    bool ready = false;
+    int sm_count = 0;
+    int occ_tiles[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    std::vector<nwap_pipe *> free_pipes;
+};
+std::mutex g_cache_mutex;
+device_cache g_cache[64];
+
+void destroy_pipe(nwap_pipe *p)
+{
+    if (!p) return;
+    cudaFree(p->d_slab[0]); cudaFree(p->d_slab[1]);
+    for (int i = 0; i < 2; ++i) {
+        if (p->ev_done[i]) cudaEventDestroy(p->ev_done[i]);
+        if (p->ev_free[i]) cudaEventDestroy(p->ev_free[i]);
+    }
+    if (p->s_compute) cudaStreamDestroy(p->s_compute);
+    if (p->s_copy) cudaStreamDestroy(p->s_copy);
+    delete p;
+}
 
 // qclass: 0 -> rows up to 16 symbols, 1 -> up to 24, 2 -> up to 32; ov: sparse-override build
 tile_kernel_t tile_kernel(int flavor, int qclass, bool ov)
@@ -89,11 +123,74 @@ tile_kernel_t tile_kernel(int flavor, int qclass, bool ov)
 }
 size_t tile_smem(bool ov) { return ov ? sizeof(nwap_tile_smem_t<true>) : sizeof(nwap_tile_smem_t<false>); }
 
+// Device facts, kernel attributes and the memory-pool policy: once per device per process.
+int ensure_device_cache(int device, device_cache **out)
+{
+    std::lock_guard<std::mutex> lock(g_cache_mutex);
+    device_cache &dc = g_cache[device];
+    if (!dc.ready) {
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        dc.sm_count = sms;
+        // the small per-context arrays come from the stream-ordered pool; keep freed blocks cached
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        unsigned long long keep = ~0ull;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        for (int f = 0; f < 4; ++f)          // f == 3: sparse-override build
+            for (int w = 0; w < 3; ++w) {
+                tile_kernel_t k = tile_kernel(f == 3 ? 1 : f, w, f == 3);
+                const size_t smem = tile_smem(f == 3);
+                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                int occ = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem));
+                dc.occ_tiles[f * 3 + w] = occ;
+            }
+        dc.ready = true;
+    }
+    *out = &dc;
+    return NWAP_OK;
+}
+
+// Small per-context device arrays: stream-ordered allocations on the legacy stream (the pool keeps
+// freed blocks, so a create/destroy cycle costs no driver allocation).
+cudaError_t dev_alloc(void *pp, size_t bytes) { return cudaMallocAsync((void **)pp, bytes, 0); }
+void dev_free(void *ptr) { if (ptr) cudaFreeAsync(ptr, 0); }
+
+// Borrow the host-destination pipeline (slabs of at least `slab` bytes) from the device cache.
+int acquire_pipe(nwap_ctx *c, int64_t slab)
+{
+    if (!c->pipe) {
+        std::lock_guard<std::mutex> lock(g_cache_mutex);
+        std::vector<nwap_pipe *> &fp = g_cache[c->device].free_pipes;
+        if (!fp.empty()) { c->pipe = fp.back(); fp.pop_back(); }
+    }
+    if (!c->pipe) {
+        nwap_pipe *p = new nwap_pipe();
+        c->pipe = p;
+        CK(cudaStreamCreateWithFlags(&p->s_compute, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&p->s_copy, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->ev_free[i], cudaEventDisableTiming));
+        }
+    }
+    nwap_pipe *p = c->pipe;
+    if (p->slab_bytes < slab) {
+        for (int i = 0; i < 2; ++i) { cudaFree(p->d_slab[i]); p->d_slab[i] = nullptr; }
+        p->slab_bytes = 0;
+        CK(cudaMalloc(&p->d_slab[0], slab));
+        CK(cudaMalloc(&p->d_slab[1], slab));
+        p->slab_bytes = slab;
+    }
+    return NWAP_OK;
+}
+
 int build_sim_table(nwap_ctx *c, const int8_t *sim_host)
 {
-    if (c->d_sim) { cudaFree(c->d_sim); c->d_sim = nullptr; }
-    CK(cudaMalloc(&c->d_sim, (size_t)c->K * c->K));
-    CK(cudaMemcpy(c->d_sim, sim_host, (size_t)c->K * c->K, cudaMemcpyHostToDevice));
+    if (c->d_sim) { CK(cudaDeviceSynchronize()); dev_free(c->d_sim); c->d_sim = nullptr; }
+    CK(dev_alloc(&c->d_sim, (size_t)c->K * c->K));
+    CK(cudaMemcpyAsync(c->d_sim, sim_host, (size_t)c->K * c->K, cudaMemcpyHostToDevice, 0));
     return NWAP_OK;
 }
 
@@ -223,6 +320,7 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
 {
     if (!ctx_out || !ids || !lengths) return fail(NWAP_EINVAL, "null argument");
     if (n < 2) return fail(NWAP_EINVAL, "need at least two words");
+    if (device < 0 || device >= 64) return fail(NWAP_EINVAL, "device %d out of range", device);
     if (q_stride < 1 || q_stride > 255) return fail(NWAP_EINVAL, "q_stride %d out of range [1, 255]", q_stride);
     int q = nwap_preflight(lengths, n, gap, std::min(match, mismatch), std::max(match, mismatch), nullptr, nullptr);
     if (q < 0) return q;
@@ -234,13 +332,16 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
         for (int j = 0; j < len; ++j) maxsym = std::max<int>(maxsym, ids[i * q_stride + j]);
     }
     CK(cudaSetDevice(device));
+    device_cache *dc = nullptr;
+    {
+        const int rc0 = ensure_device_cache(device, &dc);
+        if (rc0) return rc0;
+    }
     nwap_ctx *c = new nwap_ctx();
+    c->sm_count = dc->sm_count;
+    memcpy(c->occ_tiles, dc->occ_tiles, sizeof dc->occ_tiles);
     c->device = device; c->n = n; c->qmax = q; c->qpad = ((q + 15) / 16) * 16;
     c->match = match; c->mismatch = mismatch; c->gap = gap; c->K = maxsym + 1;
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, device));
-    c->sm_count = prop.multiProcessorCount;
-
     c->h_lens.assign(lengths, lengths + n);
     c->h_lenprefix.resize(n + 1);
     c->h_lenprefix[0] = 0;
@@ -254,15 +355,15 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
     auto guard = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess && rc == NWAP_OK) rc = fail(NWAP_ECUDA, "%s failed: %s", what, cudaGetErrorString(e));
     };
-    guard(cudaMalloc(&c->d_ids, packed.size()), "cudaMalloc(ids)");
-    guard(cudaMalloc(&c->d_lens, lens_pad), "cudaMalloc(lens)");
-    guard(cudaMalloc(&c->d_stats, sizeof(nwap_dev_stats)), "cudaMalloc(stats)");
-    guard(cudaMalloc(&c->d_counter, sizeof(unsigned long long)), "cudaMalloc(counter)");
-    guard(cudaMalloc(&c->d_total, sizeof(long long)), "cudaMalloc(total)");
+    guard(dev_alloc(&c->d_ids, packed.size()), "alloc(ids)");
+    guard(dev_alloc(&c->d_lens, lens_pad), "alloc(lens)");
+    guard(dev_alloc(&c->d_stats, sizeof(nwap_dev_stats)), "alloc(stats)");
+    guard(dev_alloc(&c->d_counter, sizeof(unsigned long long)), "alloc(counter)");
+    guard(dev_alloc(&c->d_total, sizeof(long long)), "alloc(total)");
     if (rc == NWAP_OK) {
-        guard(cudaMemcpy(c->d_ids, packed.data(), packed.size(), cudaMemcpyHostToDevice), "H2D ids");
-        guard(cudaMemset(c->d_lens, 0, lens_pad), "memset lens");
-        guard(cudaMemcpy(c->d_lens, lengths, n, cudaMemcpyHostToDevice), "H2D lens");
+        guard(cudaMemcpyAsync(c->d_ids, packed.data(), packed.size(), cudaMemcpyHostToDevice, 0), "H2D ids");
+        guard(cudaMemsetAsync(c->d_lens, 0, lens_pad, 0), "memset lens");
+        guard(cudaMemcpyAsync(c->d_lens, lengths, n, cudaMemcpyHostToDevice, 0), "H2D lens");
     }
     if (rc == NWAP_OK) {
         // uniform-scheme similarity table (engine.py:110-112) for the generic kernel
@@ -270,17 +371,8 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
         for (int k = 0; k < c->K; ++k) sim[(size_t)k * c->K + k] = (int8_t)match;
         rc = build_sim_table(c, sim.data());
     }
-    if (rc == NWAP_OK) {
-        for (int f = 0; f < 4 && rc == NWAP_OK; ++f)          // f == 3: sparse-override build
-            for (int w = 0; w < 3 && rc == NWAP_OK; ++w) {
-                tile_kernel_t k = tile_kernel(f == 3 ? 1 : f, w, f == 3);
-                const size_t smem = tile_smem(f == 3);
-                guard(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "cudaFuncSetAttribute");
-                int occ = 0;
-                guard(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem), "occupancy query");
-                c->occ_tiles[f * 3 + w] = occ;
-            }
-    }
+    // the store must be complete before kernels on other (non-blocking) streams read it
+    if (rc == NWAP_OK) guard(cudaStreamSynchronize(0), "H2D word store");
     if (rc != NWAP_OK) { nwap_destroy(c); return rc; }
     *ctx_out = c;
     return NWAP_OK;
@@ -306,28 +398,44 @@ int nwap_set_similarity(nwap_ctx *c, const int8_t *sim, int K)
     // uniform + sparse corrections?  then the packed kernel can run it
     std::vector<nwap_ov_row> tab((size_t)K);
     c->sparse_ov = K <= NWAP_OV_MAXK && nwap_build_ov_table(sim, K, c->match, c->mismatch, tab.data());
-    if (c->d_ov) { cudaFree(c->d_ov); c->d_ov = nullptr; }
+    if (c->d_ov) { CK(cudaDeviceSynchronize()); dev_free(c->d_ov); c->d_ov = nullptr; }
     if (c->sparse_ov) {
-        CK(cudaMalloc(&c->d_ov, sizeof(nwap_ov_row) * (size_t)K));
-        CK(cudaMemcpy(c->d_ov, tab.data(), sizeof(nwap_ov_row) * (size_t)K, cudaMemcpyHostToDevice));
+        CK(dev_alloc(&c->d_ov, sizeof(nwap_ov_row) * (size_t)K));
+        CK(cudaMemcpyAsync(c->d_ov, tab.data(), sizeof(nwap_ov_row) * (size_t)K, cudaMemcpyHostToDevice, 0));
     }
-    return build_sim_table(c, sim);
+    const int rc = build_sim_table(c, sim);
+    CK(cudaStreamSynchronize(0));        // tab / sim are host temporaries; other streams read the tables
+    return rc;
 }
 
 void nwap_destroy(nwap_ctx *c)
 {
     if (!c) return;
     cudaSetDevice(c->device);
-    cudaFree(c->d_ids); cudaFree(c->d_lens); cudaFree(c->d_sim); cudaFree(c->d_stats); cudaFree(c->d_ov);
-    cudaFree(c->d_counter); cudaFree(c->d_block_counts); cudaFree(c->d_total);
-    cudaFree(c->d_slab[0]); cudaFree(c->d_slab[1]);
-    for (int i = 0; i < 2; ++i) {
-        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
-        if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+    cudaDeviceSynchronize();             // nothing may still be reading the store or writing the slabs
+    dev_free(c->d_ids); dev_free(c->d_lens); dev_free(c->d_sim); dev_free(c->d_stats); dev_free(c->d_ov);
+    dev_free(c->d_counter); dev_free(c->d_block_counts); dev_free(c->d_total);
+    if (c->pipe) {                       // back to the device cache for the next context
+        std::lock_guard<std::mutex> lock(g_cache_mutex);
+        g_cache[c->device].free_pipes.push_back(c->pipe);
     }
-    if (c->s_compute) cudaStreamDestroy(c->s_compute);
-    if (c->s_copy) cudaStreamDestroy(c->s_copy);
     delete c;
+}
+
+void nwap_trim(void)
+{
+    std::lock_guard<std::mutex> lock(g_cache_mutex);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (int d = 0; d < 64; ++d) {
+        if (g_cache[d].free_pipes.empty()) continue;
+        cudaSetDevice(d);
+        for (nwap_pipe *p : g_cache[d].free_pipes) destroy_pipe(p);
+        g_cache[d].free_pipes.clear();
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    }
+    cudaSetDevice(cur);
 }
 
 int64_t nwap_num_words(const nwap_ctx *c) { return c ? c->n : 0; }
@@ -381,50 +489,58 @@ int nwap_read_stats(nwap_ctx *c, nwap_stats *stats_host, void *stream)
     return fetch_stats(c, stats_host, (cudaStream_t)stream);
 }
 
-int nwap_score_range_host(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_host, nwap_stats *stats_host,
-                          int want_hist, int variant)
+int nwap_score_range_host_begin(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_host, int want_hist, int variant)
 {
     if (!c) return fail(NWAP_EINVAL, "null context");
+    if (c->host_pending) return fail(NWAP_EINVAL, "a host-destination call is already in flight on this context");
     const int64_t P = nwap_num_edges(c);
     if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
     if (start < end && !out_host) return fail(NWAP_EINVAL, "null output buffer");
     CK(cudaSetDevice(c->device));
-    if (!c->s_compute) {
-        CK(cudaStreamCreateWithFlags(&c->s_compute, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
-        for (int i = 0; i < 2; ++i) {
-            CK(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
-        }
-    }
     const int64_t total = end - start;
     // slab: large enough to amortise launches, small enough that the first copy starts early
     int64_t slab = std::max<int64_t>(int64_t(8) << 20, std::min<int64_t>(int64_t(256) << 20, (total + 7) / 8));
     slab = (slab + 255) & ~int64_t(255);
-    if (c->slab_bytes < slab) {
-        for (int i = 0; i < 2; ++i) { cudaFree(c->d_slab[i]); c->d_slab[i] = nullptr; }
-        CK(cudaMalloc(&c->d_slab[0], slab));
-        CK(cudaMalloc(&c->d_slab[1], slab));
-        c->slab_bytes = slab;
-    }
-    int rc = reset_stats(c, c->s_compute);
+    int rc = acquire_pipe(c, slab);
+    if (rc) return rc;
+    nwap_pipe *p = c->pipe;
+    rc = reset_stats(c, p->s_compute);
     if (rc) return rc;
     int k = 0;
     for (int64_t pos = start; pos < end; pos += slab, ++k) {
         const int b = k & 1;
         const int64_t e = std::min(end, pos + slab);
-        if (k >= 2) CK(cudaStreamWaitEvent(c->s_compute, c->ev_free[b], 0));
-        rc = enqueue_score(c, pos, e, c->d_slab[b], want_hist, variant, c->s_compute);
-        if (rc) { cudaStreamSynchronize(c->s_compute); cudaStreamSynchronize(c->s_copy); return rc; }
-        CK(cudaEventRecord(c->ev_done[b], c->s_compute));
-        CK(cudaStreamWaitEvent(c->s_copy, c->ev_done[b], 0));
-        CK(cudaMemcpyAsync(out_host + (pos - start), c->d_slab[b], (size_t)(e - pos), cudaMemcpyDeviceToHost, c->s_copy));
-        CK(cudaEventRecord(c->ev_free[b], c->s_copy));
+        if (k >= 2) CK(cudaStreamWaitEvent(p->s_compute, p->ev_free[b], 0));
+        rc = enqueue_score(c, pos, e, p->d_slab[b], want_hist, variant, p->s_compute);
+        if (rc) { cudaStreamSynchronize(p->s_compute); cudaStreamSynchronize(p->s_copy); return rc; }
+        CK(cudaEventRecord(p->ev_done[b], p->s_compute));
+        CK(cudaStreamWaitEvent(p->s_copy, p->ev_done[b], 0));
+        CK(cudaMemcpyAsync(out_host + (pos - start), p->d_slab[b], (size_t)(e - pos), cudaMemcpyDeviceToHost, p->s_copy));
+        CK(cudaEventRecord(p->ev_free[b], p->s_copy));
     }
-    CK(cudaStreamSynchronize(c->s_copy));
-    if (stats_host) return fetch_stats(c, stats_host, c->s_compute);
-    CK(cudaStreamSynchronize(c->s_compute));
+    c->host_pending = true;
     return NWAP_OK;
+}
+
+int nwap_score_range_host_wait(nwap_ctx *c, nwap_stats *stats_host)
+{
+    if (!c) return fail(NWAP_EINVAL, "null context");
+    if (!c->host_pending) return fail(NWAP_EINVAL, "no host-destination call in flight on this context");
+    c->host_pending = false;
+    CK(cudaSetDevice(c->device));
+    nwap_pipe *p = c->pipe;
+    CK(cudaStreamSynchronize(p->s_copy));
+    if (stats_host) return fetch_stats(c, stats_host, p->s_compute);
+    CK(cudaStreamSynchronize(p->s_compute));
+    return NWAP_OK;
+}
+
+int nwap_score_range_host(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_host, nwap_stats *stats_host,
+                          int want_hist, int variant)
+{
+    const int rc = nwap_score_range_host_begin(c, start, end, out_host, want_hist, variant);
+    if (rc) return rc;
+    return nwap_score_range_host_wait(c, stats_host);
 }
 
 int nwap_payload_stats(nwap_ctx *c, const int8_t *payload_dev, int64_t count, nwap_stats *stats_host, void *stream)
@@ -460,8 +576,10 @@ static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start,
     const int64_t nblocks = (count + NWAP_CMP_BLOCK - 1) / NWAP_CMP_BLOCK;
     if (nblocks > 0x7fffffffLL) return fail(NWAP_EINVAL, "range too large for one compaction call; split it");
     if (c->block_counts_cap < nblocks) {
-        cudaFree(c->d_block_counts); c->d_block_counts = nullptr;
-        CK(cudaMalloc(&c->d_block_counts, sizeof(long long) * (size_t)nblocks));
+        CK(cudaDeviceSynchronize());     // an earlier compaction on another stream may still use the old scratch
+        dev_free(c->d_block_counts); c->d_block_counts = nullptr;
+        CK(dev_alloc(&c->d_block_counts, sizeof(long long) * (size_t)nblocks));
+        CK(cudaStreamSynchronize(0));
         c->block_counts_cap = nblocks;
     }
     if (mode == 0) k_compact_count<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts);

@@ -10,6 +10,7 @@ only to own device / pinned buffers and the current stream.
 from __future__ import annotations
 
 import ctypes
+import threading
 import time
 from typing import Optional, Sequence, Tuple
 
@@ -93,6 +94,7 @@ class NwapContext:
         self.device = device
         self.n = int(lengths.shape[0])
         self._h = ctypes.c_void_p()
+        self._pending = None
         L = lib()
         check(L.nwap_create(ctypes.addressof(self._h), device, ids.ctypes.data, self.n, ids.shape[1],
                             lengths.ctypes.data, match, mismatch, gap))
@@ -182,6 +184,27 @@ class NwapContext:
         st = NwapStats()
         check(lib().nwap_score_range_host(self._h, start, end, ptr, ctypes.addressof(st),
                                           int(want_hist), VARIANTS[variant]))
+        return _stats_tuple(st, want_hist)
+
+    def score_range_host_begin(self, start: int, end: int, out_host, want_hist: bool = False,
+                               variant: str = "auto") -> None:
+        """Enqueue the scoring of [start, end) into ``out_host`` and return at once; the buffer is
+        complete after :meth:`score_range_host_wait`.  One call in flight per context."""
+        ptr, size = _host_ptr(out_host)
+        if size < end - start:
+            raise ValueError("output buffer too small")
+        self._pending = (out_host, want_hist)          # keep the buffer alive until the wait
+        check(lib().nwap_score_range_host_begin(self._h, start, end, ptr, int(want_hist), VARIANTS[variant]))
+
+    def score_range_host_wait(self):
+        if self._pending is None:
+            raise ValueError("no host-destination call in flight on this context")
+        st = NwapStats()
+        _, want_hist = self._pending
+        try:
+            check(lib().nwap_score_range_host_wait(self._h, ctypes.addressof(st)))
+        finally:
+            self._pending = None
         return _stats_tuple(st, want_hist)
 
     def payload_stats(self, payload, count: Optional[int] = None):
@@ -313,19 +336,26 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
     score_max = -128
     started = time.perf_counter()
     ctx = None
+    staging = []
     try:
         ctx = NwapContext(ids, lengths, scheme, device)
         chunk = plan.chunk_size
-        # host staging slab: a whole number of sink chunks, about 64 MiB
-        slab = max(chunk, ((64 << 20) // chunk) * chunk)
+        # two pinned host slabs of a whole number of sink chunks (about 64 MiB each): the device scores
+        # and copies slab k+1 while the sink consumes slab k, in index order
+        slab = max(chunk, (_SLAB_BYTES // chunk) * chunk)
         slab = min(slab, -(-total // chunk) * chunk)
-        staging = torch.empty(slab, dtype=torch.int8).pin_memory()
-        view = memoryview(staging.numpy()).cast("B")
-        for s in range(0, total, slab):
-            e = min(s + slab, total)
-            ssum, smin, smax, scount, _ = ctx.score_range_host(s, e, staging, variant=variant)
+        ranges = [(s, min(s + slab, total)) for s in range(0, total, slab)]
+        staging = _staging_slabs(slab, 2 if len(ranges) > 1 else 1)
+        views = [memoryview(t.numpy()).cast("B") for t in staging]
+        if ranges:
+            ctx.score_range_host_begin(*ranges[0], staging[0], variant=variant)
+        for k, (s, e) in enumerate(ranges):
+            ssum, smin, smax, scount, _ = ctx.score_range_host_wait()
+            if k + 1 < len(ranges):
+                ctx.score_range_host_begin(*ranges[k + 1], staging[(k + 1) & 1], variant=variant)
             if scount != e - s:
                 raise DataError(f"device scored {scount} edges in [{s}, {e})")
+            view = views[k & 1]
             for cs in range(0, e - s, chunk):
                 piece = view[cs: min(cs + chunk, e - s)]
                 sink.write(piece)
@@ -338,10 +368,37 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
         raise
     finally:
         if ctx is not None:
-            ctx.close()
+            ctx.close()          # synchronises the device: nothing is still writing the staging slabs
+        _return_slabs(staging)
     wall = time.perf_counter() - started
     if edges != total:
         sink.abort()
         raise DataError(f"wrote {edges} edges, expected {total}")
     return ComputeStats(edges_written=edges, wall_time=wall, min_score=score_min,
                         max_score=score_max, mean_score=score_sum / edges)
+
+
+_SLAB_BYTES = 64 << 20        # host staging slab of compute_all_pairs
+_STAGING = {}
+_STAGING_LOCK = threading.Lock()
+
+
+def _staging_slabs(nbytes: int, count: int):
+    """Check out pinned host staging slabs, cached per size class (pinning 64 MiB costs ~20 ms)."""
+    import torch
+
+    size = 1 << max(16, (nbytes - 1).bit_length())
+    with _STAGING_LOCK:
+        have = _STAGING.setdefault(size, [])
+        out = [have.pop() for _ in range(min(count, len(have)))]
+    while len(out) < count:
+        out.append(torch.empty(size, dtype=torch.int8).pin_memory())
+    return out
+
+
+def _return_slabs(slabs) -> None:
+    with _STAGING_LOCK:
+        for t in slabs:
+            have = _STAGING.setdefault(t.numel(), [])
+            if len(have) < 4:
+                have.append(t)

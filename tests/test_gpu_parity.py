@@ -123,6 +123,57 @@ def test_sink_failure_aborts():
     assert sink.aborted
 
 
+def test_host_pipeline_begin_wait_and_context_cycle():
+    """The split host-destination call (two host slabs alternating, as compute_all_pairs drives it), the
+    create -> score -> destroy cycle served from the per-device cache, and nwap_trim()."""
+    ids, lens = synth.french_shaped(3000)
+    scheme = nw.ScoringScheme(1, -1, -2)
+    P = nw.num_edges(3000)
+    ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P, threads=4)
+    slabs = [torch.empty(1 << 20, dtype=torch.int8).pin_memory() for _ in range(2)]
+    for cycle in range(3):
+        with NwapContext(ids, lens, scheme) as ctx:
+            ranges = [(s, min(P, s + (1 << 20))) for s in range(0, P, 1 << 20)]
+            got = np.empty(P, dtype=np.int8)
+            tot = 0
+            ctx.score_range_host_begin(*ranges[0], slabs[0])
+            with pytest.raises(ValueError, match="already in flight"):
+                ctx.score_range_host_begin(*ranges[0], slabs[1])
+            for k, (s, e) in enumerate(ranges):
+                st = ctx.score_range_host_wait()
+                if k + 1 < len(ranges):
+                    ctx.score_range_host_begin(*ranges[k + 1], slabs[(k + 1) & 1])
+                got[s:e] = slabs[k & 1].numpy()[: e - s]
+                tot += st[0]
+                assert st[3] == e - s
+            assert np.array_equal(got, ref) and tot == rsum
+            with pytest.raises(ValueError, match="no host-destination call"):
+                ctx.score_range_host_wait()
+        if cycle == 1:
+            _native.lib().nwap_trim()          # the next context re-creates its pipeline
+
+
+def test_entry_point_with_many_slabs_matches_oracle():
+    """compute_all_pairs with more than two staging slabs in flight order (sink sees index order)."""
+    words = synth.make_words(1500, seed=77, alphabet=30, min_len=1, max_len=12)
+    scheme = nw.ScoringScheme(1, -1, -2)
+    sink = CollectSink()
+    plan = nw.ComputePlan(n=1500, chunk_size=1000, scheme=scheme)
+    import paper_2509_01654_b200.engine as eng
+    old = eng._SLAB_BYTES
+    eng._SLAB_BYTES = 200_000                   # 6 slabs of 200 chunks
+    try:
+        stats = nw.compute_all_pairs(words, scheme, sink, plan)
+    finally:
+        eng._SLAB_BYTES = old
+    wid, wl = synth.store_from_words(words)
+    ref, rsum, rmin, rmax = _oracle(wid, wl, scheme, 0, nw.num_edges(1500), threads=4)
+    assert sink.payload == ref.tobytes()
+    assert (stats.edges_written, stats.min_score, stats.max_score) == (len(ref), rmin, rmax)
+    assert stats.mean_score == rsum / len(ref)
+    assert all(len(c) == 1000 for c in sink.chunks[:-1])
+
+
 def test_errors_surface_as_reference_exceptions():
     with pytest.raises(nw.DataError, match="-280"):
         nw.compute_all_pairs([nw.EncodedWord("l", "x", tuple([0] * 70), 1.0), nw.EncodedWord("s", "y", (0, 1), 1.0)],
