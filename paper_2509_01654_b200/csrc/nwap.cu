@@ -573,7 +573,9 @@ static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start,
     if (count == 0) return NWAP_OK;
     if (!payload_dev) return fail(NWAP_EINVAL, "null payload");
     CK(cudaSetDevice(c->device));
-    const int64_t nblocks = (count + NWAP_CMP_BLOCK - 1) / NWAP_CMP_BLOCK;
+    // blocks tile the 16-byte aligned window that contains the slice (k_compact_*: nwap_cmp_first)
+    const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload_dev) & 15u);
+    const int64_t nblocks = (lead + count + NWAP_CMP_BLOCK - 1) / NWAP_CMP_BLOCK;
     if (nblocks > 0x7fffffffLL) return fail(NWAP_EINVAL, "range too large for one compaction call; split it");
     if (c->block_counts_cap < nblocks) {
         CK(cudaDeviceSynchronize());     // an earlier compaction on another stream may still use the old scratch
@@ -585,8 +587,8 @@ static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start,
     if (mode == 0) k_compact_count<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts);
     else k_compact_count<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts);
     k_compact_scan<<<1, 1024, 0, st>>>(c->d_block_counts, nblocks, c->d_total);
-    if (mode == 0) k_compact_write<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, idx_out_dev, score_out_dev, cap, degree_dev);
-    else k_compact_write<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, idx_out_dev, score_out_dev, cap, degree_dev);
+    if (mode == 0) k_compact_write<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, c->d_total, nblocks, idx_out_dev, score_out_dev, cap, degree_dev);
+    else k_compact_write<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, c->d_total, nblocks, idx_out_dev, score_out_dev, cap, degree_dev);
     g_launches += 3;
     CK(cudaGetLastError());
     long long total = 0;

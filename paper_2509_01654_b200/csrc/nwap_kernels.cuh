@@ -668,8 +668,9 @@ k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stat
 // once (fp64 estimate + integer fix-up) and then walks the triangle.
 // ---------------------------------------------------------------------------
 #define NWAP_CMP_THREADS 256
-#define NWAP_CMP_PER_THREAD 16
-#define NWAP_CMP_BLOCK (NWAP_CMP_THREADS * NWAP_CMP_PER_THREAD)   // 4096 edges per block
+#define NWAP_CMP_VEC 4                                              // 16-byte vectors per thread
+#define NWAP_CMP_PER_THREAD (16 * NWAP_CMP_VEC)                     // 64 edges per thread
+#define NWAP_CMP_BLOCK (NWAP_CMP_THREADS * NWAP_CMP_PER_THREAD)     // 16 KiB of the aligned window per block
 
 struct nwap_keep_params {
     int threshold;           // MODE 0
@@ -679,53 +680,104 @@ struct nwap_keep_params {
     int64_t start;           // linear index of payload[0]
 };
 
-// keep-bits (bit k = edge base+k kept) of one thread's run of 16 edges
-template <int MODE>
-__device__ __forceinline__ unsigned nwap_keep_bits(const int8_t *__restrict__ payload, int64_t count, int64_t base,
-                                                   const nwap_keep_params &kp, int8_t (&v)[NWAP_CMP_PER_THREAD])
+// The payload slice is scanned through its 16-byte ALIGNED window: window byte w holds edge
+// k = w - lead (lead = payload address & 15).  A thread owns 64 consecutive window bytes (four
+// LDG.128); only the first and the last vector of the whole slice can straddle its ends and are
+// assembled bytewise so nothing outside [payload, payload + count) is ever read.
+__device__ __forceinline__ uint4 nwap_cmp_load(const int8_t *__restrict__ payload, int64_t count, int64_t k0)
 {
-    unsigned bits = 0;
-    if (base >= count) {
+    if (k0 >= 0 && k0 + 16 <= count) return *reinterpret_cast<const uint4 *>(payload + k0);
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) v[k] = 0;
+    for (int j = 0; j < 16; ++j) {
+        const int64_t k = k0 + j;
+        if (k >= 0 && k < count) w[j >> 2] |= (uint32_t)(uint8_t)payload[k] << (8 * (j & 3));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// MODE 0: bit j of the result = (signed byte j of the 4 words >= threshold), 4 bytes per SWAR step.
+// x = w ^ 0x80808080 orders the bytes as unsigned; T = threshold + 128 in [0, 255].
+__device__ __forceinline__ unsigned nwap_ge_bits4(uint32_t w, uint32_t tl_rep, bool th)
+{
+    const uint32_t x = w ^ 0x80808080u;
+    const uint32_t d = ((x & 0x7f7f7f7fu) | 0x80808080u) - tl_rep;     // bit 7 of a byte: low 7 bits >= low 7 bits of T
+    const uint32_t m = (th ? (x & d) : (x | d)) & 0x80808080u;
+    return (((m >> 7) * 0x01020408u) >> 24) & 0xfu;
+}
+
+template <int MODE>
+__device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__restrict__ payload, int64_t count,
+                                                             int64_t k_first, const nwap_keep_params &kp,
+                                                             uint4 (&vec)[NWAP_CMP_VEC])
+{
+    unsigned long long bits = 0;
+    if (k_first >= count || k_first + NWAP_CMP_PER_THREAD <= 0) {
+#pragma unroll
+        for (int v = 0; v < NWAP_CMP_VEC; ++v) vec[v] = make_uint4(0u, 0u, 0u, 0u);
         return 0;
     }
-    int64_t r = 0, c = 0;
-    if (MODE == 1) {
-        r = nwap_row_of(kp.start + base, kp.n);
-        c = nwap_col_of(kp.start + base, kp.n, r);
-    }
 #pragma unroll
-    for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) {
-        const bool in = base + k < count;
-        v[k] = in ? payload[base + k] : (int8_t)0;
-        bool keep;
-        if (MODE == 0) {
-            keep = in && (int)v[k] >= kp.threshold;
-        } else {
-            keep = false;
-            if (in) {
-                const int m = max((int)kp.lens[r], (int)kp.lens[c]);
-                const double w = (100.0 * (double)v[k]) / (double)m;
-                keep = (w >= kp.lo) && (w <= kp.hi);
-                if (++c == kp.n) { ++r; c = r + 1; }
+    for (int v = 0; v < NWAP_CMP_VEC; ++v) vec[v] = nwap_cmp_load(payload, count, k_first + 16 * v);
+    // validity mask of this thread's 64 window bytes
+    unsigned long long valid = ~0ull;
+    if (k_first < 0) valid &= ~0ull << (int)(-k_first);
+    if (k_first + NWAP_CMP_PER_THREAD > count) valid &= ~0ull >> (int)(k_first + NWAP_CMP_PER_THREAD - count);
+    if (MODE == 0) {
+        const int t = kp.threshold;
+        if (t > 127) return 0;
+        if (t <= -128) return valid;
+        const uint32_t T = (uint32_t)(t + 128);
+        const uint32_t tl_rep = (T & 0x7fu) * 0x01010101u;
+        const bool th = (T & 0x80u) != 0;
+#pragma unroll
+        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+            const uint32_t w[4] = {vec[v].x, vec[v].y, vec[v].z, vec[v].w};
+            unsigned b16 = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) b16 |= nwap_ge_bits4(w[q], tl_rep, th) << (4 * q);
+            bits |= (unsigned long long)b16 << (16 * v);
+        }
+        return bits & valid;
+    }
+    // MODE 1: lo <= 100.0*score/max(len_r, len_c) <= hi in IEEE double (graph.py:96-98); (r, c) walks the triangle
+    const int64_t kb = max(k_first, (int64_t)0);
+    int64_t r = nwap_row_of(kp.start + kb, kp.n);
+    int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
+    int lr = (int)kp.lens[r];
+#pragma unroll
+    for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+        const uint32_t w[4] = {vec[v].x, vec[v].y, vec[v].z, vec[v].w};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int e = 16 * v + j;
+            if ((valid >> e) & 1ull) {
+                const int sc = (int)(int8_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                const int m = max(lr, (int)kp.lens[c]);
+                const double wgt = (100.0 * (double)sc) / (double)m;
+                if (wgt >= kp.lo && wgt <= kp.hi) bits |= 1ull << e;
+                if (++c == kp.n) { ++r; c = r + 1; lr = (int)kp.lens[min(r, kp.n - 1)]; }
             }
         }
-        bits |= (keep ? 1u : 0u) << k;
     }
     return bits;
+}
+
+// first window byte of (block, thread), as an edge offset relative to payload[0] (may be negative)
+__device__ __forceinline__ int64_t nwap_cmp_first(const int8_t *payload)
+{
+    const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload) & 15u);
+    return ((int64_t)blockIdx.x * NWAP_CMP_THREADS + threadIdx.x) * NWAP_CMP_PER_THREAD - lead;
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(NWAP_CMP_THREADS)
 k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, long long *block_counts)
 {
-    const int64_t base = (int64_t)blockIdx.x * NWAP_CMP_BLOCK + (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD;
-    int8_t v[NWAP_CMP_PER_THREAD];
-    int kept = __popc(nwap_keep_bits<MODE>(payload, count, base, kp, v));
+    uint4 vec[NWAP_CMP_VEC];
+    int kept = __popcll(nwap_keep_bits<MODE>(payload, count, nwap_cmp_first(payload), kp, vec));
     __shared__ int wsum[NWAP_CMP_THREADS / 32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    kept = __reduce_add_sync(0xffffffffu, kept);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = kept;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -773,15 +825,21 @@ k_compact_scan(long long *block_counts, int64_t nblocks, long long *total_out)
     if (threadIdx.x == 0) *total_out = carry;
 }
 
+// Blocks that keep nothing (the usual case: C5 keeps 2e-5 of the edges) return before touching the
+// payload again, so the second pass costs one read of the block offsets plus the few non-empty blocks.
 template <int MODE>
 __global__ void __launch_bounds__(NWAP_CMP_THREADS)
 k_compact_write(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp,
-                const long long *block_offsets, int64_t *idx_out, int8_t *score_out, int64_t cap, int *degree)
+                const long long *block_offsets, const long long *total, int64_t nblocks,
+                int64_t *idx_out, int8_t *score_out, int64_t cap, int *degree)
 {
-    const int64_t base = (int64_t)blockIdx.x * NWAP_CMP_BLOCK + (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD;
-    int8_t v[NWAP_CMP_PER_THREAD];
-    const unsigned bits = nwap_keep_bits<MODE>(payload, count, base, kp, v);
-    const int kept = __popc(bits);
+    const long long off0 = block_offsets[blockIdx.x];
+    const long long off1 = (int64_t)blockIdx.x + 1 < nblocks ? block_offsets[blockIdx.x + 1] : *total;
+    if (off1 == off0) return;
+    const int64_t k_first = nwap_cmp_first(payload);
+    uint4 vec[NWAP_CMP_VEC];
+    const unsigned long long bits = nwap_keep_bits<MODE>(payload, count, k_first, kp, vec);
+    const int kept = __popcll(bits);
     // exclusive scan of `kept` over the block
     __shared__ int wtot[NWAP_CMP_THREADS / 32];
     int x = kept;
@@ -794,21 +852,25 @@ k_compact_write(const int8_t *__restrict__ payload, int64_t count, const nwap_ke
     __syncthreads();
     int woff = 0;
     for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) woff += wtot[w];
-    int64_t pos = block_offsets[blockIdx.x] + woff + (x - kept);
-    if (!bits) return;
-#pragma unroll
-    for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) {
-        if ((bits >> k) & 1u) {
-            const int64_t idx = kp.start + base + k;
-            if (pos < cap) { idx_out[pos] = idx; score_out[pos] = v[k]; }
-            if (degree) {
-                const int64_t r = nwap_row_of(idx, kp.n);
-                const int64_t c = nwap_col_of(idx, kp.n, r);
-                atomicAdd(&degree[r], 1);
-                atomicAdd(&degree[c], 1);
-            }
-            ++pos;
+    int64_t pos = off0 + woff + (x - kept);
+    unsigned long long rest = bits;
+    while (rest) {
+        const int e = __ffsll((long long)rest) - 1;
+        rest &= rest - 1;
+        const int64_t idx = kp.start + k_first + e;
+        if (pos < cap) {
+            const uint4 q = vec[e >> 4];
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+            idx_out[pos] = idx;
+            score_out[pos] = (int8_t)((w4[(e >> 2) & 3] >> (8 * (e & 3))) & 0xffu);
         }
+        if (degree) {
+            const int64_t r = nwap_row_of(idx, kp.n);
+            const int64_t c = nwap_col_of(idx, kp.n, r);
+            atomicAdd(&degree[r], 1);
+            atomicAdd(&degree[c], 1);
+        }
+        ++pos;
     }
 }
 

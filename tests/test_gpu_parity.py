@@ -509,6 +509,43 @@ def test_compaction_and_degree(golden_cases):
         assert ei.value.count == int((c["payload"] >= 0).sum())
 
 
+def test_compaction_thresholds_alignments_and_tiny_ranges(golden_cases):
+    """The vectorised compaction scan: every threshold class (<= -128 keeps all, > 127 keeps none, both
+    halves of the unsigned byte order), payload pointers at every offset mod 16, ranges from 1 byte to
+    several blocks, and the normalised filter on the same slices (its (r, c) walk starts mid-vector)."""
+    c = golden_cases["seed500"]
+    n, P = 500, nw.num_edges(500)
+    lens64 = c["lengths"].astype(np.int64)
+    rng = np.random.default_rng(99)
+    with NwapContext(c["ids"], c["lengths"], _scheme(c)) as ctx:
+        big = torch.empty(P + 64, dtype=torch.int8, device="cuda")
+        for off in range(17):
+            out = big[off: off + P]
+            ctx.score_range(0, P, out)
+            spans = [(0, 1), (0, 15), (3, 20), (P - 1, P), (0, P), (16384 - off, 16384 - off + 1)]
+            spans += [tuple(sorted(rng.integers(0, P, size=2))) for _ in range(3)]
+            for s, e in spans:
+                s, e = int(s), int(e)
+                if e <= s:
+                    continue
+                thr = int(rng.choice([-200, -128, -127, -20, -3, -1, 0, 1, 2, 5, 127, 128, 300]))
+                degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+                idx, sc = ctx.compact_range(out[s:e], s, e, thr, capacity=e - s, degree=degree)
+                ridx, rsc, rdeg = orc.np_compact(c["payload"][s:e], s, n, thr)
+                assert np.array_equal(idx.cpu().numpy(), ridx), (off, s, e, thr)
+                assert np.array_equal(sc.cpu().numpy(), rsc)
+                assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
+                lo, hi = sorted(float(x) for x in rng.uniform(-120, 60, size=2))
+                idx2, sc2 = ctx.filter_normalized(out[s:e], s, e, lo, hi, capacity=e - s)
+                k = np.arange(s, e, dtype=np.int64)
+                rows = orc.np_rows_of(k, n)
+                cols = orc.np_cols_of(k, n, rows)
+                w = 100.0 * c["payload"][s:e].astype(np.float64) / np.maximum(lens64[rows], lens64[cols])
+                keep = (w >= lo) & (w <= hi)
+                assert np.array_equal(idx2.cpu().numpy(), k[keep]), (off, s, e, lo, hi)
+                assert np.array_equal(sc2.cpu().numpy(), c["payload"][s:e][keep])
+
+
 def test_c5_threshold_compaction_slab(golden_samples):
     """configs[4]: alternate scheme (2,-1,-3), keep score >= 4, on a slab of the 600k job."""
     ids, lens, sch = synth.config_store("C5")
