@@ -200,6 +200,10 @@ def main():
     ap.add_argument("--variant", default="auto", choices=["auto", "packed", "packed3", "packed_sym", "simple"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the CPU baseline sample")
     ap.add_argument("--fixed-len", type=int, default=0, help="diagnostic: all words of this length")
+    ap.add_argument("--passes", type=int, default=1,
+                    help="score each rank's shard as this many equal-work sub-shards into one reused device buffer "
+                         "(needed when the shard's int8 output exceeds HBM, e.g. --words 600000 --passes 8 on one GPU); "
+                         "no e2e leg in this mode")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -262,11 +266,26 @@ def main():
     L = _native.lib()
     sch = nw.ScoringScheme(*scheme)
     ctx = NwapContext(ids, lens, sch, device=local_rank)
-    bounds = equal_work_bounds(lens, world)
-    s0, e0 = shard_of(bounds, rank)
+    passes = max(1, args.passes)
+    bounds = equal_work_bounds(lens, world * passes)
+    s0, e0 = int(bounds[rank * passes]), int(bounds[(rank + 1) * passes])
+    sub = [(int(bounds[rank * passes + k]), int(bounds[rank * passes + k + 1])) for k in range(passes)]
     shard_pairs = e0 - s0
     shard_cells = range_cells(lens, s0, e0)
-    out = torch.empty(shard_pairs, dtype=torch.int8, device="cuda")
+    out = torch.empty(max(e - s for s, e in sub), dtype=torch.int8, device="cuda")
+    if passes > 1:
+        args.no_e2e = True
+
+    def score_shard():
+        """One step: this rank's whole shard (statistics accumulate over the sub-shards on the host side)."""
+        if passes == 1:
+            ctx.score_range(s0, e0, out, variant=args.variant, sync=False)
+            return None
+        acc = [0, 127, -128, 0]
+        for s, e in sub:
+            st = ctx.score_range(s, e, out, variant=args.variant)
+            acc = [acc[0] + st[0], min(acc[1], st[1]), max(acc[2], st[2]), acc[3] + st[3]]
+        return acc
 
     def barrier():
         if world > 1:
@@ -274,7 +293,7 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        ctx.score_range(s0, e0, out, variant=args.variant, sync=False)
+        score_shard()
     barrier()
     sampler = ClockSampler(local_rank)
     if rank == 0:
@@ -287,7 +306,7 @@ def main():
     t_start.record()
     for k in range(args.steps):
         ev[k][0].record()
-        ctx.score_range(s0, e0, out, variant=args.variant, sync=False)
+        acc = score_shard()
         ev[k][1].record()
     t_end.record()
     barrier()
@@ -295,7 +314,7 @@ def main():
     total_ms = t_start.elapsed_time(t_end)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     clocks = sampler.stop() if rank == 0 else None
-    st = ctx.read_stats()
+    st = ctx.read_stats() if passes == 1 else (acc[0], acc[1], acc[2], acc[3])
     local = ShardStats(st[0], st[3], st[1], st[2])
     tmax = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -310,7 +329,7 @@ def main():
     # ---- roofline of the dominant kernel (k_score_tiles): integer issue bound -------------
     roof = None
     if rank == 0:
-        kern_ms = float(np.mean(step_ms))                 # one k_score_tiles launch per step (+1 tiny init)
+        kern_ms = float(np.mean(step_ms))                 # `passes` k_score_tiles launches per step (+ tiny inits)
         # the packed cell's exact instruction mix (auto resolves to packed3 for a uniform scheme)
         mix_name, instr_per_cell, mix_desc = {
             "packed": ("mix_2alu_2imad", 4, "2 DPX + 2 IMAD"),
@@ -332,7 +351,7 @@ def main():
             "achieved": achieved, "peak": peak_gcups, "unit": "GCUPS", "frac": achieved / peak_gcups,
             "traffic": traffic_from_profile(n),
             "kernel": "k_score_tiles", "kernel_ms": kern_ms,
-            "algorithmic_bytes": int(shard_pairs),
+            "algorithmic_bytes": int(shard_pairs), "launches_per_step": passes,
             "peak_how": (f"live probe {mix_name}: {ipc_mix:.3f} warp-instr/clk/SM on the packed cell's own "
                          f"{instr_per_cell}-instruction mix ({mix_desc}) x {cells_per_instr:.2f} cells/instr x {SM_COUNT} SMs x "
                          f"{sm_max:.0f} MHz (clocks.max.sm); "
@@ -408,7 +427,7 @@ def main():
         "config": {"workload": wname, "words": n, "pairs": P, "cells": cells_total, "variant": args.variant,
                    "l2": "output written per step (>= 5 GB per GPU) exceeds the 126 MB L2; the 3 MB word store is "
                          "L2/shared-memory resident by design",
-                   "sharding": f"{world} equal-work contiguous shard(s)"},
+                   "sharding": f"{world} equal-work contiguous shard(s)" + (f", each scored as {passes} sub-shards into one reused buffer" if passes > 1 else "")},
         "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
         "stats": {"sum": tot.sum, "min": tot.min, "max": tot.max, "count": tot.count},
         "step_ms": step_ms,
