@@ -5,7 +5,7 @@
 takes the reference's ``phonsim compute`` arguments (cli.py:75-85), prints the same four lines
 (cli.py:184-190), writes the same ``.nwedges`` + manifest files and uses the same exit codes
 (cli.py:13: 0 success, 1 usage error, 2 data error, 3 I/O error).  ``--workers`` is accepted and
-ignored (one process drives one GPU); ``--device`` picks the GPU.  Scheme files (``--scheme``,
+ignored; ``--device`` picks the GPU, ``--devices 0,1,...`` shares the edge range between several.  Scheme files (``--scheme``,
 parsed by aligner.py:195-239) belong to the reference's text front end and are not re-implemented:
 pass overrides through the Python API instead.  Every other ``phonsim`` sub-command works on the
 finished store and stays with the reference.
@@ -44,6 +44,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--workers", type=int, default=1, help="accepted for compatibility, ignored")
     p.add_argument("--chunk-size", type=int, default=DEFAULT_CHUNK_SIZE)
     p.add_argument("--device", type=int, default=0, help="CUDA device index")
+    p.add_argument("--devices", default=None, help="comma-separated CUDA device indices to share the work (default: --device)")
     p.add_argument("--out", required=True, help="output prefix for the edge store")
     p.set_defaults(func=cmd_compute)
     return parser
@@ -57,12 +58,16 @@ def cmd_compute(args) -> int:
     if args.scheme:
         raise UsageError("scheme files are not supported by the GPU front end; use --match/--mismatch/--gap "
                          "or the Python API (ScoringScheme(overrides=...))")
+    try:
+        devices = [int(d) for d in args.devices.split(",")] if args.devices else [args.device]
+    except ValueError:
+        raise UsageError("devices must be a comma-separated list of integers") from None
     words = load_words(args.words_file)
     scheme = ScoringScheme(args.match, args.mismatch, args.gap)
     preflight_range_check(words, scheme)            # fail before any output file exists (cli.py:177)
     plan = ComputePlan(n=len(words), chunk_size=args.chunk_size, worker_count=args.workers, scheme=scheme)
     writer = PipelinedEdgeStoreWriter(args.out, words, scheme)
-    stats = compute_all_pairs(words, scheme, writer, plan, device=args.device)
+    stats = compute_all_pairs(words, scheme, writer, plan, devices=devices)
     manifest = writer.finalize()
     print(f"computed {stats.edges_written} edges in {stats.wall_time:.2f} s")
     print(f"scores: min {stats.min_score}, max {stats.max_score}, mean {stats.mean_score:.4f}")

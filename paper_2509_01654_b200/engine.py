@@ -308,12 +308,20 @@ def probe(which: str, iters: int = 2000, device: int = 0):
 
 
 def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan] = None,
-                      device: int = 0, variant: str = "auto") -> ComputeStats:
+                      device: int = 0, variant: str = "auto",
+                      devices: Optional[Sequence[int]] = None) -> ComputeStats:
     """Drop-in for reference engine.py:218-290.
 
     Every edge score goes through ``sink.write`` once, in linear-index order, in
     pieces of ``plan.chunk_size`` edges (the payload never depends on it); on any
     failure ``sink.abort()`` is called before the exception propagates.
+
+    ``devices`` (default ``[device]``) lists the GPUs to use from this one process -- the
+    counterpart of the reference's fork pool (engine.py:262-276): slab k of the edge range
+    is scored by GPU ``k mod G`` into that GPU's own pinned staging slabs, and the sink
+    consumes the slabs in index order, so the payload is the same for any G
+    (partition invariance, tests/test_engine.py:92-101).  The word store is replicated; no
+    edge byte moves between GPUs.
     """
     import torch
 
@@ -325,6 +333,9 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
         raise ValueError(f"plan is for n={plan.n}, got {n} words")
     if not same_scheme(plan.scheme, scheme):
         raise ValueError("plan scheme differs from the scheme argument")
+    devs = [int(d) for d in (devices if devices is not None else [device])]
+    if not devs:
+        raise ValueError("devices must name at least one GPU")
     if not torch.cuda.is_available():
         raise RuntimeError("compute_all_pairs needs a CUDA device: there is no CPU fallback")
 
@@ -335,27 +346,36 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
     score_min = 127
     score_max = -128
     started = time.perf_counter()
-    ctx = None
-    staging = []
+    ctxs: list = []
+    staging: list = []
     try:
-        ctx = NwapContext(ids, lengths, scheme, device)
         chunk = plan.chunk_size
-        # two pinned host slabs of a whole number of sink chunks (about 64 MiB each): the device scores
-        # and copies slab k+1 while the sink consumes slab k, in index order
+        # pinned host slabs of a whole number of sink chunks (about 64 MiB each), two per GPU: the devices
+        # score and copy the next slabs while the sink consumes slab k, in index order
         slab = max(chunk, (_SLAB_BYTES // chunk) * chunk)
         slab = min(slab, -(-total // chunk) * chunk)
         ranges = [(s, min(s + slab, total)) for s in range(0, total, slab)]
-        staging = _staging_slabs(slab, 2 if len(ranges) > 1 else 1)
+        G = max(1, min(len(devs), len(ranges)))
+        ctxs = [NwapContext(ids, lengths, scheme, d) for d in devs[:G]]
+        per_gpu = 2 if len(ranges) > G else 1
+        staging = _staging_slabs(slab, G * per_gpu)
         views = [memoryview(t.numpy()).cast("B") for t in staging]
-        if ranges:
-            ctx.score_range_host_begin(*ranges[0], staging[0], variant=variant)
+
+        def buf(k):                       # staging slab of range k: GPU k mod G, its buffer (k div G) mod 2
+            return (k % G) * per_gpu + ((k // G) % per_gpu)
+
+        def begin(k):
+            ctxs[k % G].score_range_host_begin(*ranges[k], staging[buf(k)], variant=variant)
+
+        for k in range(min(G, len(ranges))):
+            begin(k)
         for k, (s, e) in enumerate(ranges):
-            ssum, smin, smax, scount, _ = ctx.score_range_host_wait()
-            if k + 1 < len(ranges):
-                ctx.score_range_host_begin(*ranges[k + 1], staging[(k + 1) & 1], variant=variant)
+            ssum, smin, smax, scount, _ = ctxs[k % G].score_range_host_wait()
+            if k + G < len(ranges):
+                begin(k + G)
             if scount != e - s:
                 raise DataError(f"device scored {scount} edges in [{s}, {e})")
-            view = views[k & 1]
+            view = views[buf(k)]
             for cs in range(0, e - s, chunk):
                 piece = view[cs: min(cs + chunk, e - s)]
                 sink.write(piece)
@@ -367,8 +387,8 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
         sink.abort()
         raise
     finally:
-        if ctx is not None:
-            ctx.close()          # synchronises the device: nothing is still writing the staging slabs
+        for c in ctxs:
+            c.close()            # synchronises the device: nothing is still writing the staging slabs
         _return_slabs(staging)
     wall = time.perf_counter() - started
     if edges != total:
@@ -400,5 +420,5 @@ def _return_slabs(slabs) -> None:
     with _STAGING_LOCK:
         for t in slabs:
             have = _STAGING.setdefault(t.numel(), [])
-            if len(have) < 4:
+            if len(have) < 16:
                 have.append(t)

@@ -174,6 +174,35 @@ def test_entry_point_with_many_slabs_matches_oracle():
     assert all(len(c) == 1000 for c in sink.chunks[:-1])
 
 
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_entry_point_shares_slabs_between_contexts(devices):
+    """The single-process multi-GPU path of compute_all_pairs (slab k -> device k mod G), exercised with
+    several contexts on the one GPU this box has: same payload, statistics and chunking for any G."""
+    words = synth.make_words(1200, seed=5, alphabet=25, min_len=1, max_len=14)
+    scheme = nw.ScoringScheme(2, -1, -2)
+    plan = nw.ComputePlan(n=1200, chunk_size=4096, scheme=scheme)
+    import paper_2509_01654_b200.engine as eng
+    old = eng._SLAB_BYTES
+    eng._SLAB_BYTES = 100_000                   # 30 slabs of 24 chunks
+    try:
+        sink = CollectSink()
+        stats = nw.compute_all_pairs(words, scheme, sink, plan, devices=devices)
+        bad = CollectSink(fail_at=40)
+        with pytest.raises(OSError):
+            nw.compute_all_pairs(words, scheme, bad, plan, devices=devices)
+        assert bad.aborted
+    finally:
+        eng._SLAB_BYTES = old
+    wid, wl = synth.store_from_words(words)
+    ref, rsum, rmin, rmax = _oracle(wid, wl, scheme, 0, nw.num_edges(1200), threads=4)
+    assert sink.payload == ref.tobytes()
+    assert (stats.edges_written, stats.min_score, stats.max_score) == (len(ref), rmin, rmax)
+    assert stats.mean_score == rsum / len(ref)
+    assert all(len(c) == 4096 for c in sink.chunks[:-1])
+    with pytest.raises(ValueError, match="at least one GPU"):
+        nw.compute_all_pairs(words, scheme, CollectSink(), plan, devices=[])
+
+
 def test_errors_surface_as_reference_exceptions():
     with pytest.raises(nw.DataError, match="-280"):
         nw.compute_all_pairs([nw.EncodedWord("l", "x", tuple([0] * 70), 1.0), nw.EncodedWord("s", "y", (0, 1), 1.0)],
