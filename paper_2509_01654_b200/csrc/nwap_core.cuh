@@ -205,6 +205,10 @@ struct nwap_sym2 { uint32_t a2, left0; };
 #ifndef NWAP_PREFETCH
 #define NWAP_PREFETCH 0
 #endif
+//   NWAP_DUFF_MAXLB n: length bodies up to n run two matrix rows per loop trip (0 = off)
+#ifndef NWAP_DUFF_MAXLB
+#define NWAP_DUFF_MAXLB 0
+#endif
 
 template <int LB, int FLAVOR>
 NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
@@ -223,6 +227,28 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
         } while (s != e);
         return;
     }
+#if NWAP_DUFF_MAXLB > 0
+    if (LB <= NWAP_DUFF_MAXLB) {
+        // two matrix rows per loop trip; an odd word enters at the second copy (the update is in place, so
+        // both copies are the same code on the same registers)
+        if (la & 1) goto second_row;
+#pragma unroll 1
+        do {
+            {
+                const nwap_sym2 x = *s++;
+                nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+                d0 = x.left0;
+            }
+        second_row:
+            {
+                const nwap_sym2 x = *s++;
+                nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+                d0 = x.left0;
+            }
+        } while (s != e);
+        return;
+    }
+#endif
 #if NWAP_PREFETCH
     nwap_sym2 x = *s;
 #pragma unroll 1
