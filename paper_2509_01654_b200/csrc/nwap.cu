@@ -167,20 +167,29 @@ int acquire_pipe(nwap_ctx *c, int64_t slab)
     }
     if (!c->pipe) {
         nwap_pipe *p = new nwap_pipe();
-        c->pipe = p;
-        CK(cudaStreamCreateWithFlags(&p->s_compute, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&p->s_copy, cudaStreamNonBlocking));
-        for (int i = 0; i < 2; ++i) {
-            CK(cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&p->ev_free[i], cudaEventDisableTiming));
+        cudaError_t e = cudaStreamCreateWithFlags(&p->s_compute, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_copy, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&p->ev_done[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_free[i], cudaEventDisableTiming);
         }
+        if (e != cudaSuccess) {          // never cache a half-built pipeline
+            destroy_pipe(p);
+            return fail(NWAP_ECUDA, "creating the host-destination pipeline failed: %s", cudaGetErrorString(e));
+        }
+        c->pipe = p;
     }
     nwap_pipe *p = c->pipe;
     if (p->slab_bytes < slab) {
         for (int i = 0; i < 2; ++i) { cudaFree(p->d_slab[i]); p->d_slab[i] = nullptr; }
         p->slab_bytes = 0;
-        CK(cudaMalloc(&p->d_slab[0], slab));
-        CK(cudaMalloc(&p->d_slab[1], slab));
+        for (int i = 0; i < 2; ++i) {
+            const cudaError_t e = cudaMalloc(&p->d_slab[i], slab);
+            if (e != cudaSuccess) {
+                for (int k = 0; k < 2; ++k) { cudaFree(p->d_slab[k]); p->d_slab[k] = nullptr; }
+                return fail(NWAP_ECUDA, "cudaMalloc of a %lld-byte device slab failed: %s", (long long)slab, cudaGetErrorString(e));
+            }
+        }
         p->slab_bytes = slab;
     }
     return NWAP_OK;

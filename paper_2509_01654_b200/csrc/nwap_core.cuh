@@ -205,6 +205,11 @@ struct nwap_sym2 { uint32_t a2, left0; };
 #ifndef NWAP_PREFETCH
 #define NWAP_PREFETCH 0
 #endif
+//   NWAP_PEEL 1: the first matrix row is peeled (H'[0][j] = BIAS is folded in: no row initialisation,
+//                no up+u add in that row), the loop runs the remaining la-1 rows
+#ifndef NWAP_PEEL
+#define NWAP_PEEL 0
+#endif
 //   NWAP_DUFF_MAXLB n: length bodies up to n run two matrix rows per loop trip (0 = off)
 #ifndef NWAP_DUFF_MAXLB
 #define NWAP_DUFF_MAXLB 0
@@ -214,6 +219,30 @@ template <int LB, int FLAVOR>
 NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
                           uint32_t (&P)[LB + 1], const nwap_scheme_consts &sc)
 {
+#if NWAP_PEEL
+    if (FLAVOR == 1) {
+        // matrix row 1: every H'[0][j] is BIAS, so diag and up+u are constants and nothing is read from P
+        const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
+        const nwap_sym2 x0 = *s++;
+        const uint32_t bu = NWAP_BIAS2 + sc.u2;
+        uint32_t left = x0.left0;
+        P[0] = NWAP_BIAS2;
+#pragma unroll
+        for (int j = 1; j <= LB; ++j) {
+            const uint32_t dw = nwap_viaddmin_u16x2(x0.a2, nb[j - 1], 0x00010001u) * sc.neg_delta + NWAP_BIAS2;
+            left = nwap_vimax3_s16x2(dw, bu, left);
+            P[j] = left;
+        }
+        uint32_t d0 = x0.left0;
+#pragma unroll 1
+        while (s != e) {
+            const nwap_sym2 x = *s++;
+            nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+            d0 = x.left0;
+        }
+        return;
+    }
+#endif
 #pragma unroll
     for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;        // H'[0][j]
     uint32_t d0 = NWAP_BIAS2;                               // H'[0][0]

@@ -20,13 +20,17 @@
 #endif
 
 // Tile geometry (compile-time): a band is R rows, a strip is C columns.
+// 320 threads = 10 warps per CTA, two CTAs per SM: the warps of a CTA pull neighbouring chunks of the
+// length-sorted strip, so at any moment an SM executes two or three of the 32 length-specialised
+// bodies instead of up to twenty (5 CTAs x 4 warps did): the instruction-cache cliff that bounded
+// every larger-code variant moves away (profiles/r01h_ab_big_cta.txt).
 #ifndef NWAP_THREADS
-#define NWAP_THREADS 128       // threads per CTA of the tile kernel
+#define NWAP_THREADS 320       // threads per CTA of the tile kernel
 #endif
 #ifndef NWAP_R
 #define NWAP_R 16
 #endif
-#define NWAP_C (16 * NWAP_THREADS)   // one aligned uint4 of lengths per thread: 2048 columns
+#define NWAP_C (16 * NWAP_THREADS)   // one aligned uint4 of lengths per thread: 5120 columns
 #define NWAP_CHUNK 64          // sorted columns per warp chunk (2 per lane)
 
 NWAP_HD int64_t nwap_before_row(int64_t r, int64_t n) { return (r * (2 * n - r - 1)) >> 1; }

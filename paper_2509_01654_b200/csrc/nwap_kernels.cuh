@@ -25,10 +25,10 @@
 #define NWAP_LBSTEP 1
 #endif
 #ifndef NWAP_MINB
-#define NWAP_MINB 5               // resident CTAs/SM the register allocator must allow (Q <= 24)
+#define NWAP_MINB 2               // resident CTAs/SM the register allocator must allow
 #endif
 #ifndef NWAP_UNITS_PER_SLOT
-#define NWAP_UNITS_PER_SLOT 24
+#define NWAP_UNITS_PER_SLOT 48
 #endif
 #define NWAP_WARPS (NWAP_THREADS / 32)
 #define NWAP_PITCH (NWAP_C + 16)         // bytes per staged output row (multiple of 16)
@@ -276,6 +276,51 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
     nwap_close_chunk(ls, ca);
 }
 
+// NWAP_HOIST=1 (default): the length dispatch is done once per chunk and each length body owns the
+// whole row loop with the emit inlined.  With 4-warp CTAs this lost 13-18 % to instruction-cache
+// misses (profiles/r01e); with 10-warp CTAs it gains 3-4 % (profiles/r01h_ab_big_cta.txt).
+// NWAP_HOIST=0 keeps the per-row dispatch with one shared epilogue.
+#ifndef NWAP_HOIST
+#define NWAP_HOIST 1
+#endif
+template <int LB, int FLAVOR, class SM>
+__device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
+                                                  const nwap_lane_cols &c, int mixmode, bool fast, int want_hist,
+                                                  nwap_lane_stats &ls, nwap_chunk_acc &ca)
+{
+    const bool deep = mixmode > 2;
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;
+        uint32_t v, vm1, vm2;
+        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+}
+
+template <int FLAVOR, int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                 const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                 const nwap_lane_cols &c, int mixmode, bool fast,
+                                                 int want_hist, nwap_lane_stats &ls)
+{
+    uint32_t nb[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb_f<FLAVOR>(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_chunk_rows_h<(n <= QMAX ? n : 1), FLAVOR>(sm, sc, nb, c, mixmode, fast, want_hist, ls, ca); \
+        break;
+    switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+    nwap_close_chunk(ls, ca);
+}
+
+
 // Tried and rejected this round (same-box A/B, evidence in profiles/r01c..r01e and git history):
 // hoisting the length dispatch out of the row loop, one symbol stream per band, dual-chain
 // chunks (4 columns per lane), a cold code family for chunks spanning >= 3 lengths.
@@ -293,7 +338,7 @@ __device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
 // accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
 template <int FLAVOR, int QMAX, bool OV>
-__global__ void __launch_bounds__(NWAP_THREADS, (OV ? 4 : (QMAX <= 24 ? NWAP_MINB : (NWAP_MINB > 4 ? 4 : NWAP_MINB))))
+__global__ void __launch_bounds__(NWAP_THREADS, NWAP_MINB)
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -462,7 +507,11 @@ k_score_tiles(const nwap_tile_params p)
                 const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
                 const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
                 const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
+#if NWAP_HOIST
+                nwap_run_chunk_h<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+#else
                 nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+#endif
             }
             __syncthreads();
 
