@@ -40,13 +40,17 @@ inst = [float(r[ix["Instructions Executed"]]) for r in data]
 pos = {a: i for i, a in enumerate(addr)}
 tot_s, tot_i = sum(samp), sum(inst)
 inloop = [False] * len(data)
+back = []
 for i, t in enumerate(text):
     m = re.search(r"BRA\s+(?:P\d, )?0x([0-9a-f]+)", t)
     if m:
         tgt = int(m.group(1), 16)
-        if tgt < addr[i] and tgt in pos and i - pos[tgt] < 200 and any("VIMNMX3" in text[k] for k in range(pos[tgt], i + 1)):
-            for k in range(pos[tgt], i + 1):
-                inloop[k] = True
+        if tgt < addr[i] and tgt in pos:
+            back.append((i - pos[tgt], pos[tgt], i))
+for _, j, i in sorted(back):                       # innermost loops first: only they count as matrix-row loops
+    if i - j < 200 and any("VIMNMX3" in text[k] for k in range(j, i + 1)) and not any(inloop[k] for k in range(j, i + 1)):
+        for k in range(j, i + 1):
+            inloop[k] = True
 cell = re.compile(r"(VIMNMX3|VIADDMNMX|IMAD R\d+, R\d+, UR|VIADD R\d+, R\d+, UR|IADD3 R\d+, PT, PT, -R)")
 first = min(k for k, f in enumerate(inloop) if f)
 last = max(k for k, f in enumerate(inloop) if f)
@@ -62,9 +66,9 @@ regions = [
     ("DP matrix-row loops (all length bodies)", [k for k in range(len(data)) if inloop[k]]),
     ("  of which the four DP-cell instructions", [k for k in range(len(data)) if inloop[k] and cell.match(text[k])]),
     ("  of which loop control (LDS, pointer, test, move, branch)", [k for k in range(len(data)) if inloop[k] and not cell.match(text[k])]),
-    ("before the bodies: unit/band/chunk set-up, row head, length dispatch", list(range(0, first))),
-    ("between loops: row-init, deep select, jumps to the shared epilogue", [k for k in range(first, last + 1) if not inloop[k]]),
-    ("after the bodies: emit (score fix-up, stage store, statistics), flush, reductions", list(range(last + 1, len(data)))),
+    ("before the bodies: unit/band/chunk set-up, column fetch, length dispatch", list(range(0, first))),
+    ("inside the bodies, outside the matrix-row loops: row head, row init, select, emit", [k for k in range(first, last + 1) if not inloop[k]]),
+    ("after the bodies: flush, end-of-band barrier, reductions", list(range(last + 1, len(data)))),
 ]
 for name, keys in regions:
     s, i = share(keys)
