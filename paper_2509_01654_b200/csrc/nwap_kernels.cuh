@@ -96,7 +96,6 @@ struct nwap_tile_smem_t {
     int mn, mx;
     int ncols;
     int next_chunk;
-    int band_simple;      // every staged row is valid over the whole sorted column window
 };
 
 typedef nwap_tile_smem_t<false> nwap_tile_smem;
@@ -465,19 +464,17 @@ k_score_tiles(const nwap_tile_params p)
             }
             if (tid == 0) sm.next_chunk = 0;
             __syncthreads();
-            if (tid == 0) {
-                // simple band: all R rows present and each covers the whole sorted column window
-                int simple = !p.want_hist;
-                for (int rr = 0; rr < NWAP_R; ++rr)
-                    simple &= (sm.meta[rr].la > 0) && (sm.meta[rr].clo_off <= win_lo) &&
-                              (sm.meta[rr].clo_off + sm.meta[rr].seglen >= win_hi);
-                sm.band_simple = simple;
-            }
-            __syncthreads();
+            // simple band: all R rows present and each covers the whole sorted column window, i.e. the band lies
+            // entirely to the left of the strip (every row r has r + 1 <= strip_lo, so its columns start at the
+            // strip's first column) and neither end of the launch range clips one of its rows.  Evaluated by
+            // every thread from launch scalars: no extra barrier, nothing read back from shared memory.
+            const bool clip_first = p.r_first >= rb0 && p.r_first < rb0 + NWAP_R && p.c_start > strip_lo;
+            const bool clip_last = p.r_last >= rb0 && p.r_last < rb0 + NWAP_R && p.c_end + 1 < strip_hi;
+            const bool band_simple = !p.want_hist && rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax &&
+                                     rb0 + NWAP_R - 1 < strip_lo && !clip_first && !clip_last;
 
             // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
             const int ncols = sm.ncols;
-            const bool band_simple = sm.band_simple != 0;
             for (;;) {
                 int item = 0;
                 if (lane == 0) item = atomicAdd(&sm.next_chunk, 1);

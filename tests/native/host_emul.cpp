@@ -14,6 +14,7 @@ static uint32_t run_pair(const uint8_t *a, int la, const uint8_t *b0, int lb0,
     for (int i = 0; i < la; ++i) {
         row2[i].a2 = (uint32_t)a[i] * sc.symmul;
         row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+
     }
     uint32_t nb[LB];
     for (int j = 0; j < LB; ++j)
