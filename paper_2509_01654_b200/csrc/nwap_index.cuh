@@ -33,6 +33,17 @@
 #define NWAP_C (16 * NWAP_THREADS)   // one aligned uint4 of lengths per thread: 5120 columns
 #define NWAP_CHUNK 64          // sorted columns per warp chunk (2 per lane)
 
+// floor(num / m) for |num| <= 12800, 1 <= m <= 255 from one IEEE single-precision division (exact in this
+// range: see k_hist_normalized).  Replaces store.py:360's integer floor division on the device.
+NWAP_HD int nwap_floor_div_small(int num, int m)
+{
+#if defined(__CUDA_ARCH__)
+    return __float2int_rd(__fdiv_rn((float)num, (float)m));
+#else
+    return (int)floorf((float)num / (float)m);
+#endif
+}
+
 NWAP_HD int64_t nwap_before_row(int64_t r, int64_t n) { return (r * (2 * n - r - 1)) >> 1; }
 
 // Row of linear index idx, 0 <= idx < n(n-1)/2.

@@ -720,11 +720,30 @@ k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stat
 
 struct nwap_keep_params {
     int threshold;           // MODE 0
-    double lo, hi;           // MODE 1
     const uint8_t *lens;     // MODE 1
     int64_t n;
     int64_t start;           // linear index of payload[0]
+    // MODE 1: for every m = max(len_r, len_c) the scores s with lo <= 100.0*s/m <= hi form an interval
+    // [smin[m], smax[m]] (the quotient is monotonic in s).  The host fills the table by evaluating the
+    // reference's IEEE-double expression (graph.py:96-98) for all 256 x 255 (s, m), so the device test is
+    // two integer compares and exactly the reference's keep-mask; an empty interval is smin > smax.
+    int8_t smin[256], smax[256];
 };
+
+// host side of the table above
+inline void nwap_fill_norm_bounds(nwap_keep_params &kp, double lo, double hi)
+{
+    for (int m = 0; m < 256; ++m) {
+        int first = 1, last = 0;                     // empty
+        bool any = false;
+        for (int sc = -128; sc <= 127 && m > 0; ++sc) {
+            const double w = (100.0 * (double)sc) / (double)m;
+            if (w >= lo && w <= hi) { if (!any) first = sc; last = sc; any = true; }
+        }
+        kp.smin[m] = (int8_t)first;
+        kp.smax[m] = (int8_t)last;
+    }
+}
 
 // The payload slice is scanned through its 16-byte ALIGNED window: window byte w holds edge
 // k = w - lead (lead = payload address & 15).  A thread owns 64 consecutive window bytes (four
@@ -755,7 +774,7 @@ __device__ __forceinline__ unsigned nwap_ge_bits4(uint32_t w, uint32_t tl_rep, b
 template <int MODE>
 __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__restrict__ payload, int64_t count,
                                                              int64_t k_first, const nwap_keep_params &kp,
-                                                             uint4 (&vec)[NWAP_CMP_VEC])
+                                                             uint4 (&vec)[NWAP_CMP_VEC], const short2 *bounds)
 {
     unsigned long long bits = 0;
     if (k_first >= count || k_first + NWAP_CMP_PER_THREAD <= 0) {
@@ -786,7 +805,8 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
         }
         return bits & valid;
     }
-    // MODE 1: lo <= 100.0*score/max(len_r, len_c) <= hi in IEEE double (graph.py:96-98); (r, c) walks the triangle
+    // MODE 1: lo <= 100.0*score/max(len_r, len_c) <= hi (graph.py:96-98) through the per-length score
+    // bounds in shared memory; (r, c) walks the triangle
     const int64_t kb = max(k_first, (int64_t)0);
     int64_t r = nwap_row_of(kp.start + kb, kp.n);
     int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
@@ -799,9 +819,8 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
             const int e = 16 * v + j;
             if ((valid >> e) & 1ull) {
                 const int sc = (int)(int8_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                const int m = max(lr, (int)kp.lens[c]);
-                const double wgt = (100.0 * (double)sc) / (double)m;
-                if (wgt >= kp.lo && wgt <= kp.hi) bits |= 1ull << e;
+                const short2 b = bounds[max(lr, (int)kp.lens[c])];
+                if (sc >= (int)b.x && sc <= (int)b.y) bits |= 1ull << e;
                 if (++c == kp.n) { ++r; c = r + 1; lr = (int)kp.lens[min(r, kp.n - 1)]; }
             }
         }
@@ -820,8 +839,13 @@ template <int MODE>
 __global__ void __launch_bounds__(NWAP_CMP_THREADS)
 k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, long long *block_counts)
 {
+    __shared__ short2 bounds[MODE == 1 ? 256 : 1];
+    if (MODE == 1) {
+        bounds[threadIdx.x] = make_short2(kp.smin[threadIdx.x], kp.smax[threadIdx.x]);     // NWAP_CMP_THREADS == 256
+        __syncthreads();
+    }
     uint4 vec[NWAP_CMP_VEC];
-    int kept = __popcll(nwap_keep_bits<MODE>(payload, count, nwap_cmp_first(payload), kp, vec));
+    int kept = __popcll(nwap_keep_bits<MODE>(payload, count, nwap_cmp_first(payload), kp, vec, bounds));
     __shared__ int wsum[NWAP_CMP_THREADS / 32];
     kept = __reduce_add_sync(0xffffffffu, kept);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = kept;
@@ -833,7 +857,9 @@ k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_ke
     }
 }
 
-// single-CTA exclusive scan of block_counts (in place); total -> *total_out
+// single-CTA exclusive scan of block_counts (in place); total -> *total_out.  Each thread owns 8 consecutive
+// counts per trip (8192 per trip), so a 2 GiB slice (131,072 blocks) is 16 trips.
+#define NWAP_SCAN_PER 8
 __global__ void __launch_bounds__(1024)
 k_compact_scan(long long *block_counts, int64_t nblocks, long long *total_out)
 {
@@ -841,10 +867,16 @@ k_compact_scan(long long *block_counts, int64_t nblocks, long long *total_out)
     __shared__ long long carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int64_t base = 0; base < nblocks; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        long long v = i < nblocks ? block_counts[i] : 0;
-        long long x = v;
+    for (int64_t base = 0; base < nblocks; base += 1024 * NWAP_SCAN_PER) {
+        const int64_t i0 = base + (int64_t)threadIdx.x * NWAP_SCAN_PER;
+        long long v[NWAP_SCAN_PER];
+        long long tsum = 0;
+#pragma unroll
+        for (int k = 0; k < NWAP_SCAN_PER; ++k) {
+            v[k] = i0 + k < nblocks ? block_counts[i0 + k] : 0;
+            tsum += v[k];
+        }
+        long long x = tsum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             long long y = __shfl_up_sync(0xffffffffu, x, o);
@@ -862,10 +894,14 @@ k_compact_scan(long long *block_counts, int64_t nblocks, long long *total_out)
             wtot[threadIdx.x] = ws - w;      // exclusive warp offsets
         }
         __syncthreads();
-        const long long excl = carry + wtot[threadIdx.x >> 5] + (x - v);
-        if (i < nblocks) block_counts[i] = excl;
+        long long run = carry + wtot[threadIdx.x >> 5] + (x - tsum);
+#pragma unroll
+        for (int k = 0; k < NWAP_SCAN_PER; ++k) {
+            if (i0 + k < nblocks) block_counts[i0 + k] = run;
+            run += v[k];
+        }
         __syncthreads();
-        if (threadIdx.x == 1023) carry = excl + v;
+        if (threadIdx.x == 1023) carry = run;
         __syncthreads();
     }
     if (threadIdx.x == 0) *total_out = carry;
@@ -882,9 +918,14 @@ k_compact_write(const int8_t *__restrict__ payload, int64_t count, const nwap_ke
     const long long off0 = block_offsets[blockIdx.x];
     const long long off1 = (int64_t)blockIdx.x + 1 < nblocks ? block_offsets[blockIdx.x + 1] : *total;
     if (off1 == off0) return;
+    __shared__ short2 bounds[MODE == 1 ? 256 : 1];
+    if (MODE == 1) {
+        bounds[threadIdx.x] = make_short2(kp.smin[threadIdx.x], kp.smax[threadIdx.x]);
+        __syncthreads();
+    }
     const int64_t k_first = nwap_cmp_first(payload);
     uint4 vec[NWAP_CMP_VEC];
-    const unsigned long long bits = nwap_keep_bits<MODE>(payload, count, k_first, kp, vec);
+    const unsigned long long bits = nwap_keep_bits<MODE>(payload, count, k_first, kp, vec, bounds);
     const int kept = __popcll(bits);
     // exclusive scan of `kept` over the block
     __shared__ int wtot[NWAP_CMP_THREADS / 32];
@@ -936,21 +977,36 @@ k_hist_normalized(const int8_t *__restrict__ payload, int64_t count, const nwap_
     extern __shared__ unsigned int sbins[];
     for (int b = threadIdx.x; b < NWAP_NHIST_SPAN; b += blockDim.x) sbins[b] = 0;
     __syncthreads();
-    // each CTA takes a contiguous slice; each thread walks runs of 16 edges
-    const int64_t runs = (count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
+    // The slice is read through its 16-byte aligned window, 64 edges (four LDG.128) per thread per trip, as in
+    // the compaction scan.  floor(100*s / m) is taken from an IEEE single division: |100*s| <= 12800 and
+    // m <= 255 are exact floats, an integral quotient is exact, and a non-integral one is at least 1/255 away
+    // from the next integer (relative 3e-7 > 2^-24), so rounding never reaches it; checked exhaustively on the
+    // host for all 256 x 255 (s, m) in tests/test_core_emul.py.
+    const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload) & 15u);
+    const int64_t runs = (lead + count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
     for (int64_t run = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; run < runs; run += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t base = run * NWAP_CMP_PER_THREAD;
-        int64_t r = nwap_row_of(kp.start + base, kp.n);
-        int64_t c = nwap_col_of(kp.start + base, kp.n, r);
+        const int64_t k_first = run * NWAP_CMP_PER_THREAD - lead;
+        const int64_t kb = max(k_first, (int64_t)0);
+        if (kb >= count) continue;
+        int64_t r = nwap_row_of(kp.start + kb, kp.n);
+        int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
+        int lr = (int)kp.lens[r];
 #pragma unroll
-        for (int k = 0; k < NWAP_CMP_PER_THREAD; ++k) {
-            if (base + k < count) {
-                const int m = max((int)kp.lens[r], (int)kp.lens[c]);
-                const int num = 100 * (int)payload[base + k];
-                int q = num / m;
-                if ((num % m != 0) && (num < 0)) --q;           // floor division
-                atomicAdd(&sbins[q - NWAP_NHIST_OFFSET], 1u);
-                if (++c == kp.n) { ++r; c = r + 1; }
+        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+            const int64_t k0 = k_first + 16 * v;
+            if (k0 + 16 <= 0 || k0 >= count) continue;
+            const uint4 q4 = nwap_cmp_load(payload, count, k0);
+            const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int64_t k = k0 + j;
+                if (k >= 0 && k < count) {
+                    const int m = max(lr, (int)kp.lens[c]);
+                    const int num = 100 * (int)(int8_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                    const int q = nwap_floor_div_small(num, m);
+                    atomicAdd(&sbins[q - NWAP_NHIST_OFFSET], 1u);
+                    if (++c == kp.n) { ++r; c = r + 1; lr = (int)kp.lens[min(r, kp.n - 1)]; }
+                }
             }
         }
     }

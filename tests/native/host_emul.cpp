@@ -115,5 +115,7 @@ void emul_unit_decode(int64_t n, int gb, int64_t t, int64_t *group, int64_t *str
     nwap_unit_decode(u, t, group, strip);
 }
 
+int emul_floor_div_small(int num, int m) { return nwap_floor_div_small(num, m); }
+
 int emul_geometry(int *R, int *C, int *chunk) { *R = NWAP_R; *C = NWAP_C; *chunk = NWAP_CHUNK; return 0; }
 }

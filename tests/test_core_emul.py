@@ -125,6 +125,14 @@ def test_sparse_override_rows_match_oracle(emul):
     assert checked > 3500 and dense < 100
 
 
+def test_small_floor_division_is_exact(emul):
+    """k_hist_normalized takes floor(100*score / max_len) (store.py:360) from one single-precision division:
+    exhaustive over every int8 score and every length 1..255."""
+    for s in range(-128, 128):
+        for m in range(1, 256):
+            assert emul.emul_floor_div_small(100 * s, m) == (100 * s) // m, (s, m)
+
+
 def test_device_index_recovery_matches_reference(emul, golden_triangle):
     t = golden_triangle
     for n in (4, 300, 10 ** 5, 10 ** 6, 10 ** 7, 600_000):
