@@ -62,13 +62,14 @@ struct nwap_tile_params {
     int ov_K;
 };
 
-struct nwap_row_meta {
+struct alignas(16) nwap_row_meta {
+    // first 16 bytes: everything the fast row path needs, one LDS.128
     int la;            // row word length, 0 = row not in this launch / no valid column in this strip
     uint32_t ala2;     // (alpha * la) * 65537: the row potential, packed for both halves
-    int clo_off;       // first valid column, relative to the strip
-    int seglen;        // number of valid columns in this strip for this row
     int rowadj;        // smem byte index of (column offset 0): rr*PITCH + skew - clo_off
     int skew;          // (global address of the segment) & 15
+    int clo_off;       // first valid column, relative to the strip
+    int seglen;        // number of valid columns in this strip for this row
     int64_t g0;        // out-relative byte offset of the segment
 };
 
@@ -85,7 +86,7 @@ struct nwap_tile_smem_t {
     typedef typename nwap_sym_of<OV>::type sym_t;
     alignas(16) sym_t rowsym[NWAP_R][NWAP_MAXLEN_FAST + 1];      // {a*65537, H'[i+1][0] (, override row)} per matrix row
     alignas(16) nwap_ov_row ov[OV ? NWAP_OV_MAXK : 1];              // per-symbol override table (sparse-override mode)
-    nwap_row_meta meta[NWAP_R];
+    alignas(16) nwap_row_meta meta[NWAP_R];
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
     uint8_t clen[NWAP_C];         // their lengths
     int bins[NWAP_WARPS][NWAP_MAXLEN_FAST + 2];
@@ -288,12 +289,29 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
 #ifndef NWAP_HOIST_FASTONLY
 #define NWAP_HOIST_FASTONLY 1
 #endif
+#ifndef NWAP_ROW_PREFETCH
+#define NWAP_ROW_PREFETCH 1
+#endif
 template <int LB, int FLAVOR, class SM>
 __device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
                                                   const nwap_lane_cols &c, int mixmode, bool fast, int want_hist,
                                                   nwap_lane_stats &ls, nwap_chunk_acc &ca)
 {
     const bool deep = mixmode > 2;
+#if NWAP_HOIST_FASTONLY && NWAP_ROW_PREFETCH
+    // every row of a fast chunk is live: fetch the next row's {la, ala2, rowadj} (one LDS.128) a row ahead
+    uint4 nxt = *reinterpret_cast<const uint4 *>(&sm.meta[0]);
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const uint4 cur = nxt;
+        nxt = *reinterpret_cast<const uint4 *>(&sm.meta[rr + 1 < NWAP_R ? rr + 1 : rr]);
+        uint32_t v, vm1, vm2;
+        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, (int)cur.x, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+        nwap_emit(sm, sm.meta[rr], cur.y, (int)cur.z, v, c, nwap_true(), 0, ls, ca);
+    }
+    return;
+#endif
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
         const nwap_row_meta &m = sm.meta[rr];
