@@ -794,6 +794,24 @@ __device__ __forceinline__ uint4 nwap_cmp_load(const int8_t *__restrict__ payloa
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// lens[c0 .. c0+63] as 16 packed words from 17 aligned 32-bit loads and byte permutes.  A thread's 64 edges of one
+// row are 64 consecutive columns; fetching their lengths bytewise costs one L1 sector per lane per byte (lanes
+// are 64 B apart), which made the normalised-weight kernels L1-bound.  Reads at most 3 bytes past c0+63: the
+// device copy of lens is zero-padded by a whole strip.
+__device__ __forceinline__ void nwap_load_lens64(const uint8_t *__restrict__ lens, int64_t c0, uint32_t (&V)[16])
+{
+    const uintptr_t a = reinterpret_cast<uintptr_t>(lens + c0);
+    const uint32_t *p = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
+    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(a & 3u);
+    uint32_t w = __ldg(p);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t nx = __ldg(p + j + 1);
+        V[j] = __byte_perm(w, nx, sel);
+        w = nx;
+    }
+}
+
 // MODE 0: bit j of the result = (signed byte j of the 4 words >= threshold), 4 bytes per SWAR step.
 // x = w ^ 0x80808080 orders the bytes as unsigned; T = threshold + 128 in [0, 255].
 __device__ __forceinline__ unsigned nwap_ge_bits4(uint32_t w, uint32_t tl_rep, bool th)
@@ -844,6 +862,24 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
     int64_t r = nwap_row_of(kp.start + kb, kp.n);
     int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
     int lr = (int)kp.lens[r];
+    if (valid == ~0ull && c + NWAP_CMP_PER_THREAD <= kp.n) {
+        // the usual case: 64 live edges of one row = 64 consecutive columns
+        uint32_t L[16];
+        nwap_load_lens64(kp.lens, c, L);
+#pragma unroll
+        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+            const uint32_t w[4] = {vec[v].x, vec[v].y, vec[v].z, vec[v].w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int e = 16 * v + j;
+                const int sc = (int)(int8_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                const int lc = (int)((L[e >> 2] >> (8 * (e & 3))) & 0xffu);
+                const short2 b = bounds[max(lr, lc)];
+                if (sc >= (int)b.x && sc <= (int)b.y) bits |= 1ull << e;
+            }
+        }
+        return bits;
+    }
 #pragma unroll
     for (int v = 0; v < NWAP_CMP_VEC; ++v) {
         const uint32_t w[4] = {vec[v].x, vec[v].y, vec[v].z, vec[v].w};
@@ -1024,6 +1060,24 @@ k_hist_normalized(const int8_t *__restrict__ payload, int64_t count, const nwap_
         int64_t r = nwap_row_of(kp.start + kb, kp.n);
         int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
         int lr = (int)kp.lens[r];
+        if (k_first >= 0 && k_first + NWAP_CMP_PER_THREAD <= count && c + NWAP_CMP_PER_THREAD <= kp.n) {
+            // the usual case: 64 live edges of one row = 64 consecutive columns (vector loads for both streams)
+            uint32_t L[16];
+            nwap_load_lens64(kp.lens, c, L);
+#pragma unroll
+            for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+                const uint4 q4 = *reinterpret_cast<const uint4 *>(payload + k_first + 16 * v);
+                const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int e = 16 * v + j;
+                    const int m = max(lr, (int)((L[e >> 2] >> (8 * (e & 3))) & 0xffu));
+                    const int num = 100 * (int)(int8_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                    atomicAdd(&sbins[nwap_floor_div_small(num, m) - NWAP_NHIST_OFFSET], 1u);
+                }
+            }
+            continue;
+        }
 #pragma unroll
         for (int v = 0; v < NWAP_CMP_VEC; ++v) {
             const int64_t k0 = k_first + 16 * v;
