@@ -515,10 +515,14 @@ int nwap_score_range_host_begin(nwap_ctx *c, int64_t start, int64_t end, int8_t 
     nwap_pipe *p = c->pipe;
     rc = reset_stats(c, p->s_compute);
     if (rc) return rc;
+    // the first two slabs are short (16 MB, 64 MB) so the first device->host copy starts after ~0.1 ms of
+    // scoring instead of ~1.7 ms; from then on the copy engine is the bottleneck and never idles
     int k = 0;
-    for (int64_t pos = start; pos < end; pos += slab, ++k) {
+    for (int64_t pos = start; pos < end; ++k) {
         const int b = k & 1;
-        const int64_t e = std::min(end, pos + slab);
+        const int64_t this_slab = k == 0 ? std::min<int64_t>(slab, int64_t(16) << 20)
+                                : k == 1 ? std::min<int64_t>(slab, int64_t(64) << 20) : slab;
+        const int64_t e = std::min(end, pos + this_slab);
         if (k >= 2) CK(cudaStreamWaitEvent(p->s_compute, p->ev_free[b], 0));
         rc = enqueue_score(c, pos, e, p->d_slab[b], want_hist, variant, p->s_compute);
         if (rc) { cudaStreamSynchronize(p->s_compute); cudaStreamSynchronize(p->s_copy); return rc; }
@@ -526,6 +530,7 @@ int nwap_score_range_host_begin(nwap_ctx *c, int64_t start, int64_t end, int8_t 
         CK(cudaStreamWaitEvent(p->s_copy, p->ev_done[b], 0));
         CK(cudaMemcpyAsync(out_host + (pos - start), p->d_slab[b], (size_t)(e - pos), cudaMemcpyDeviceToHost, p->s_copy));
         CK(cudaEventRecord(p->ev_free[b], p->s_copy));
+        pos = e;
     }
     c->host_pending = true;
     return NWAP_OK;
