@@ -1,11 +1,12 @@
 // nwap_kernels.cuh -- sm_100a kernels of the all-pairs NW scoring path.
 //
-//   k_score_tiles<FLAVOR,QMAX>  the hot kernel: persistent CTAs over (strip, band-group)
-//                               work units; per unit the strip's columns are counting-sorted
-//                               by word length in shared memory, warps pull 64-column chunks
-//                               longest-first, each lane scores 2 pairs per register (s16x2
-//                               DPX), results are staged in shared memory at their ORIGINAL
-//                               column and flushed as coalesced 16-byte stores.
+//   k_score_tiles<FLAVOR,QMAX>  the hot kernel: persistent 10-warp CTAs (two per SM) over (strip, band-group)
+//                               work units; per unit the strip's 5120 columns are counting-sorted by word
+//                               length in shared memory, warps pull 64-column chunks longest-first (so the
+//                               warps of a CTA sit in neighbouring length-specialised bodies), each lane
+//                               scores 2 pairs per register (s16x2 DPX); one length dispatch per chunk, the
+//                               body owning the loop over the band's 16 rows; results are staged in shared
+//                               memory at their ORIGINAL column and flushed as coalesced 16-byte stores.
 //                               Replaces reference engine.py:176-195 (_score_range) with
 //                               triangle.py:93-112 folded in (one index recovery per row).
 //   k_score_simple              one thread per pair, int32 cells, K x K similarity table:
