@@ -293,45 +293,40 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
 #ifndef NWAP_ROW_PREFETCH
 #define NWAP_ROW_PREFETCH 1
 #endif
-template <int LB, int FLAVOR, class SM>
+template <int LB, int FLAVOR, bool FASTONLY, class SM>
 __device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
                                                   const nwap_lane_cols &c, int mixmode, bool fast, int want_hist,
                                                   nwap_lane_stats &ls, nwap_chunk_acc &ca)
 {
     const bool deep = mixmode > 2;
-#if NWAP_HOIST_FASTONLY && NWAP_ROW_PREFETCH
-    // every row of a fast chunk is live: fetch the next row's {la, ala2, rowadj} (one LDS.128) a row ahead
-    uint4 nxt = *reinterpret_cast<const uint4 *>(&sm.meta[0]);
+    if (FASTONLY && NWAP_ROW_PREFETCH) {
+        // every row of a fast chunk is live: fetch the next row's {la, ala2, rowadj} (one LDS.128) a row ahead
+        uint4 nxt = *reinterpret_cast<const uint4 *>(&sm.meta[0]);
 #pragma unroll 1
-    for (int rr = 0; rr < NWAP_R; ++rr) {
-        const uint4 cur = nxt;
-        nxt = *reinterpret_cast<const uint4 *>(&sm.meta[rr + 1 < NWAP_R ? rr + 1 : rr]);
-        uint32_t v, vm1, vm2;
-        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, (int)cur.x, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
-        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
-        nwap_emit(sm, sm.meta[rr], cur.y, (int)cur.z, v, c, nwap_true(), 0, ls, ca);
+        for (int rr = 0; rr < NWAP_R; ++rr) {
+            const uint4 cur = nxt;
+            nxt = *reinterpret_cast<const uint4 *>(&sm.meta[rr + 1 < NWAP_R ? rr + 1 : rr]);
+            uint32_t v, vm1, vm2;
+            nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, (int)cur.x, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+            if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+            nwap_emit(sm, sm.meta[rr], cur.y, (int)cur.z, v, c, nwap_true(), 0, ls, ca);
+        }
+        return;
     }
-    return;
-#endif
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
-#if !NWAP_HOIST_FASTONLY
-        if (la == 0) continue;
-#endif
+        if (!FASTONLY && la == 0) continue;
         uint32_t v, vm1, vm2;
         nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
         if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
-#if NWAP_HOIST_FASTONLY
-        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, nwap_true(), 0, ls, ca);
-#else
-        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
-#endif
+        if (FASTONLY) nwap_emit(sm, m, m.ala2, m.rowadj, v, c, nwap_true(), 0, ls, ca);
+        else nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
     }
 }
 
-template <int FLAVOR, int QMAX, int QW, class SM>
+template <int FLAVOR, int QMAX, int QW, bool FASTONLY, class SM>
 __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_scheme_consts &sc,
                                                  const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
                                                  const nwap_lane_cols &c, int mixmode, bool fast,
@@ -343,7 +338,7 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
-        if (n <= QMAX) nwap_chunk_rows_h<(n <= QMAX ? n : 1), FLAVOR>(sm, sc, nb, c, mixmode, fast, want_hist, ls, ca); \
+        if (n <= QMAX) nwap_chunk_rows_h<(n <= QMAX ? n : 1), FLAVOR, FASTONLY>(sm, sc, nb, c, mixmode, fast, want_hist, ls, ca); \
         break;
     switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
@@ -368,7 +363,7 @@ __device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
 // accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
 template <int FLAVOR, int QMAX, bool OV>
-__global__ void __launch_bounds__(NWAP_THREADS, NWAP_MINB)
+__global__ void __launch_bounds__(NWAP_THREADS, ((OV && QMAX > 24) ? 1 : NWAP_MINB))   // the 32-wide sparse-override build needs > 96 registers
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -535,11 +530,12 @@ k_score_tiles(const nwap_tile_params p)
                 const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
                 const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
                 const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
-#if NWAP_HOIST && NWAP_HOIST_FASTONLY
-                if (fast) nwap_run_chunk_h<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+#if NWAP_HOIST
+                // two code families only where the register budget allows (the 32-wide and sparse-override
+                // instantiations would spill): there the hoisted bodies also carry the slow emit
+                constexpr bool FASTONLY = NWAP_HOIST_FASTONLY && QMAX <= 24 && !OV;
+                if (!FASTONLY || fast) nwap_run_chunk_h<FLAVOR, QMAX, QW, FASTONLY>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
                 else nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
-#elif NWAP_HOIST
-                nwap_run_chunk_h<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
 #else
                 nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
 #endif
