@@ -24,6 +24,30 @@ def _allowed(variants, scheme):
     return [v for v in variants if v != "packed_sym" or ok]
 
 
+@pytest.mark.parametrize("n", [5119, 5120, 5121, 10241])
+def test_strip_boundary_sizes(n):
+    """Vocabulary sizes around whole strips of the tile kernel (5120 columns): ragged last strip of 1 column,
+    exactly full strips, one column over; every byte and the statistics against the oracle, plus a range that
+    starts and ends mid-row next to a strip boundary."""
+    rng = np.random.default_rng(n)
+    lens = np.clip(np.rint(rng.normal(8.5, 2.8, size=n)), 1, 24).astype(np.uint8)
+    ids = rng.integers(0, 40, size=(n, 24)).astype(np.uint8)
+    scheme = nw.ScoringScheme(1, -1, -2)
+    P = nw.num_edges(n)
+    ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P, threads=len(__import__("os").sched_getaffinity(0)))
+    with NwapContext(ids, lens, scheme) as ctx:
+        out = torch.empty(P, dtype=torch.int8, device="cuda")
+        st = ctx.score_range(0, P, out)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        assert st[:4] == (rsum, rmin, rmax, P)
+        s = nw.index_of(7, 5118, n)
+        e = nw.index_of(3000, n - 2, n) if n > 3002 else P
+        got, st2 = _score(ctx, s, e, "auto", offset=5)
+        assert np.array_equal(got, ref[s:e])
+        sub = ref[s:e].astype(np.int64)
+        assert st2[:4] == (int(sub.sum()), int(sub.min()), int(sub.max()), e - s)
+
+
 class CollectSink:
     def __init__(self, fail_at=None):
         self.chunks, self.aborted, self.fail_at = [], False, fail_at
