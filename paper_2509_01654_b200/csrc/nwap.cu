@@ -594,13 +594,17 @@ static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start,
     if (c->block_counts_cap < nblocks) {
         CK(cudaDeviceSynchronize());     // an earlier compaction on another stream may still use the old scratch
         dev_free(c->d_block_counts); c->d_block_counts = nullptr;
-        CK(dev_alloc(&c->d_block_counts, sizeof(long long) * (size_t)nblocks));
+        // block counts, then one total per scan group behind them
+        CK(dev_alloc(&c->d_block_counts, sizeof(long long) * (size_t)(nblocks + (nblocks + NWAP_SCAN_GROUP - 1) / NWAP_SCAN_GROUP)));
         CK(cudaStreamSynchronize(0));
         c->block_counts_cap = nblocks;
     }
-    if (mode == 0) k_compact_count<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts);
-    else k_compact_count<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts);
-    k_compact_scan<<<1, 1024, 0, st>>>(c->d_block_counts, nblocks, c->d_total);
+    const int64_t ngroups = (nblocks + NWAP_SCAN_GROUP - 1) / NWAP_SCAN_GROUP;
+    unsigned long long *group_totals = reinterpret_cast<unsigned long long *>(c->d_block_counts + c->block_counts_cap);
+    CK(cudaMemsetAsync(group_totals, 0, sizeof(unsigned long long) * (size_t)ngroups, st));
+    if (mode == 0) k_compact_count<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, group_totals);
+    else k_compact_count<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, group_totals);
+    k_compact_scan<<<(unsigned)ngroups, 1024, 0, st>>>(c->d_block_counts, nblocks, group_totals, ngroups, c->d_total);
     if (mode == 0) k_compact_write<0><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, c->d_total, nblocks, idx_out_dev, score_out_dev, cap, degree_dev);
     else k_compact_write<1><<<(unsigned)nblocks, NWAP_CMP_THREADS, 0, st>>>(payload_dev, count, kp, c->d_block_counts, c->d_total, nblocks, idx_out_dev, score_out_dev, cap, degree_dev);
     g_launches += 3;

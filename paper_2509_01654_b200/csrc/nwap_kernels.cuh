@@ -747,6 +747,8 @@ k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stat
 #define NWAP_CMP_VEC 4                                              // 16-byte vectors per thread
 #define NWAP_CMP_PER_THREAD (16 * NWAP_CMP_VEC)                     // 64 edges per thread
 #define NWAP_CMP_BLOCK (NWAP_CMP_THREADS * NWAP_CMP_PER_THREAD)     // 16 KiB of the aligned window per block
+#define NWAP_SCAN_PER 8                                             // block counts per thread of the scan
+#define NWAP_SCAN_GROUP (1024 * NWAP_SCAN_PER)                      // block counts per scan CTA
 
 struct nwap_keep_params {
     int threshold;           // MODE 0
@@ -903,7 +905,8 @@ __device__ __forceinline__ int64_t nwap_cmp_first(const int8_t *payload)
 
 template <int MODE>
 __global__ void __launch_bounds__(NWAP_CMP_THREADS)
-k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, long long *block_counts)
+k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, long long *block_counts,
+                unsigned long long *group_totals)
 {
     __shared__ short2 bounds[MODE == 1 ? 256 : 1];
     if (MODE == 1) {
@@ -920,57 +923,71 @@ k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_ke
         int tot = 0;
         for (int w = 0; w < NWAP_CMP_THREADS / 32; ++w) tot += wsum[w];
         block_counts[blockIdx.x] = tot;
+        if (tot) atomicAdd(&group_totals[blockIdx.x / NWAP_SCAN_GROUP], (unsigned long long)tot);   // kept edges are rare
     }
 }
 
-// single-CTA exclusive scan of block_counts (in place); total -> *total_out.  Each thread owns 8 consecutive
-// counts per trip (8192 per trip), so a 2 GiB slice (131,072 blocks) is 16 trips.
-#define NWAP_SCAN_PER 8
+// Exclusive scan of block_counts (in place), one CTA per group of NWAP_SCAN_GROUP counts: the group's base is
+// the sum of the totals of the groups before it (accumulated by k_compact_count), then a local scan with 8
+// consecutive counts per thread.  CTA 0 also writes the grand total.
 __global__ void __launch_bounds__(1024)
-k_compact_scan(long long *block_counts, int64_t nblocks, long long *total_out)
+k_compact_scan(long long *block_counts, int64_t nblocks, const unsigned long long *group_totals, int64_t ngroups,
+               long long *total_out)
 {
     __shared__ long long wtot[32];
-    __shared__ long long carry;
-    if (threadIdx.x == 0) carry = 0;
+    __shared__ long long base_s;
+    // base = sum of group_totals[0 .. blockIdx.x)  (and the grand total in CTA 0)
+    long long part = 0, all = 0;
+    for (int64_t g = threadIdx.x; g < ngroups; g += 1024) {
+        const long long v = (long long)group_totals[g];
+        if (g < (int64_t)blockIdx.x) part += v;
+        all += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { part += __shfl_xor_sync(0xffffffffu, part, o); all += __shfl_xor_sync(0xffffffffu, all, o); }
+    if ((threadIdx.x & 31) == 0) wtot[threadIdx.x >> 5] = part;
     __syncthreads();
-    for (int64_t base = 0; base < nblocks; base += 1024 * NWAP_SCAN_PER) {
-        const int64_t i0 = base + (int64_t)threadIdx.x * NWAP_SCAN_PER;
-        long long v[NWAP_SCAN_PER];
-        long long tsum = 0;
-#pragma unroll
-        for (int k = 0; k < NWAP_SCAN_PER; ++k) {
-            v[k] = i0 + k < nblocks ? block_counts[i0 + k] : 0;
-            tsum += v[k];
-        }
-        long long x = tsum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            long long y = __shfl_up_sync(0xffffffffu, x, o);
-            if ((threadIdx.x & 31) >= o) x += y;
-        }
-        if ((threadIdx.x & 31) == 31) wtot[threadIdx.x >> 5] = x;
+    if (threadIdx.x == 0) { long long b = 0; for (int w = 0; w < 32; ++w) b += wtot[w]; base_s = b; }
+    __syncthreads();
+    if (blockIdx.x == 0) {
         __syncthreads();
-        if (threadIdx.x < 32) {
-            long long w = wtot[threadIdx.x], ws = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                long long y = __shfl_up_sync(0xffffffffu, ws, o);
-                if (threadIdx.x >= o) ws += y;
-            }
-            wtot[threadIdx.x] = ws - w;      // exclusive warp offsets
-        }
+        if ((threadIdx.x & 31) == 0) wtot[threadIdx.x >> 5] = all;
         __syncthreads();
-        long long run = carry + wtot[threadIdx.x >> 5] + (x - tsum);
-#pragma unroll
-        for (int k = 0; k < NWAP_SCAN_PER; ++k) {
-            if (i0 + k < nblocks) block_counts[i0 + k] = run;
-            run += v[k];
-        }
-        __syncthreads();
-        if (threadIdx.x == 1023) carry = run;
+        if (threadIdx.x == 0) { long long t = 0; for (int w = 0; w < 32; ++w) t += wtot[w]; *total_out = t; }
         __syncthreads();
     }
-    if (threadIdx.x == 0) *total_out = carry;
+    const int64_t i0 = (int64_t)blockIdx.x * NWAP_SCAN_GROUP + (int64_t)threadIdx.x * NWAP_SCAN_PER;
+    long long v[NWAP_SCAN_PER];
+    long long tsum = 0;
+#pragma unroll
+    for (int k = 0; k < NWAP_SCAN_PER; ++k) {
+        v[k] = i0 + k < nblocks ? block_counts[i0 + k] : 0;
+        tsum += v[k];
+    }
+    long long x = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) wtot[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        long long w = wtot[threadIdx.x], ws = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (threadIdx.x >= o) ws += y;
+        }
+        wtot[threadIdx.x] = ws - w;      // exclusive warp offsets
+    }
+    __syncthreads();
+    long long run = base_s + wtot[threadIdx.x >> 5] + (x - tsum);
+#pragma unroll
+    for (int k = 0; k < NWAP_SCAN_PER; ++k) {
+        if (i0 + k < nblocks) block_counts[i0 + k] = run;
+        run += v[k];
+    }
 }
 
 // Blocks that keep nothing (the usual case: C5 keeps 2e-5 of the edges) return before touching the
