@@ -44,6 +44,8 @@ extern "C" {
 #define NWAP_VARIANT_SIMPLE  1  /* one thread per pair, int32 cells, K x K table: any scheme, any q <= 255 */
 #define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 DPX + 2 IMAD per packed cell */
 #define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 2 DPX + 1 IMAD + 1 IADD per packed cell */
+#define NWAP_VARIANT_PACKED_TAB 5 /* s16x2 DPX tile kernel with a K x K similarity table in shared memory (K <= 128):
+                                   * dense override tables; 2 byte loads per packed cell instead of compare + multiply */
 #define NWAP_VARIANT_PACKED_SYM 4 /* s16x2 DPX tile kernel, symmetric gap potential: 2 DPX + 1 IADD3 per packed cell
                                    * (needs match >= mismatch and no overrides) */
 
@@ -86,8 +88,9 @@ int nwap_create(nwap_ctx **ctx_out, int device,
 /* ScoringScheme.overrides (aligner.py:51-65, engine.py:113-116): install a
  * dense symmetric K x K similarity table (host int8, row-major).  Symbols >= K
  * are rejected.  If the table is the uniform scheme plus at most 3 overrides per symbol
- * (and K <= 128) the packed kernel still runs it (sparse-override mode); otherwise scoring is
- * routed through the table-driven generic kernel. */
+ * (and K <= 128) the packed kernel still runs it (sparse-override mode); a denser table with
+ * K <= 128 runs on the packed kernel's table-driven flavour (NWAP_VARIANT_PACKED_TAB);
+ * anything else is routed through the generic one-thread-per-pair kernel. */
 int nwap_set_similarity(nwap_ctx *ctx, const int8_t *sim, int K);
 
 void nwap_destroy(nwap_ctx *ctx);

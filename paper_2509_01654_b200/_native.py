@@ -16,7 +16,7 @@ LIB_PATH = Path(os.environ["NWAP_LIB"]).resolve() if os.environ.get("NWAP_LIB") 
 
 NWAP_OK, NWAP_EINVAL, NWAP_ERANGE, NWAP_ECUDA, NWAP_ENOMEM, NWAP_ECAPACITY = 0, -1, -2, -3, -4, -5
 VARIANT_AUTO, VARIANT_SIMPLE, VARIANT_PACKED, VARIANT_PACKED3 = 0, 1, 2, 3
-VARIANTS = {"auto": 0, "simple": 1, "packed": 2, "packed3": 3, "packed_sym": 4}
+VARIANTS = {"auto": 0, "simple": 1, "packed": 2, "packed3": 3, "packed_sym": 4, "packed_tab": 5}
 PROBES = ["viaddmnmx_u16x2", "vimnmx3_s16x2", "vimnmx_s16x2", "imad", "lop3", "iadd3",
           "mix_2alu_2imad", "mix_3alu_1imad", "viadd_16x2", "vimnmx_u16x2_min", "hfma2", "hmnmx2", "prmt",
           "pair_dpx_iadd", "pair_dpx_vimnmx2", "pair_imad_iadd", "pair_imad_hfma2", "pair_dpx_imad",

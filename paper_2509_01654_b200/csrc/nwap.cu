@@ -42,7 +42,7 @@ int fail(int code, const char *fmt, ...)
     } while (0)
 
 static_assert(sizeof(nwap_dev_stats) == sizeof(nwap_stats), "stats layouts must agree");
-static_assert(sizeof(nwap_tile_smem_t<true>) <= 227 * 1024, "tile shared memory too large");
+static_assert(sizeof(nwap_tile_smem_t<1>) <= 227 * 1024 && sizeof(nwap_tile_smem_t<2>) <= 227 * 1024, "tile shared memory too large");
 
 }  // namespace
 
@@ -57,6 +57,9 @@ struct nwap_ctx {
     bool general = false;  // explicit similarity table installed
     bool sparse_ov = false; // ... and it is uniform + at most NWAP_MAX_OV overrides per symbol (packed kernel can run it)
     nwap_ov_row *d_ov = nullptr;
+    bool tab_ok = false;    // ... or it is dense but K <= 128: the packed kernel's table-driven flavour runs it
+    int tab_max = 0;        // the table's maximum M (the table on the device holds M - sim)
+    uint8_t *d_etab = nullptr;
     std::vector<uint8_t> h_lens;        // host copy for shard arithmetic
     std::vector<int64_t> h_lenprefix;   // prefix sums of lengths (n+1)
     uint8_t *d_ids = nullptr;
@@ -71,7 +74,7 @@ struct nwap_ctx {
     // host-destination pipeline: borrowed from the per-device cache on first use, returned in nwap_destroy
     struct nwap_pipe *pipe = nullptr;
     bool host_pending = false;          // nwap_score_range_host_begin issued, nwap_score_range_host_wait not yet
-    int occ_tiles[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor | ov=3, qclass) instantiation
+    int occ_tiles[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor 0..2 | ov=3 | table=4, qclass) instantiation
 };
 
 // Two device slabs, two streams and four events: everything nwap_score_range_host needs to overlap
@@ -94,7 +97,7 @@ typedef void (*tile_kernel_t)(const nwap_tile_params);
 struct device_cache {
     bool ready = false;
     int sm_count = 0;
-    int occ_tiles[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int occ_tiles[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     std::vector<nwap_pipe *> free_pipes;
 };
 std::mutex g_cache_mutex;
@@ -119,9 +122,11 @@ tile_kernel_t tile_kernel(int flavor, int qclass, bool ov)
     if (ov) return qclass == 0 ? k_score_tiles<1, 16, true> : qclass == 1 ? k_score_tiles<1, 24, true> : k_score_tiles<1, 32, true>;
     if (flavor == 0) return qclass == 0 ? k_score_tiles<0, 16, false> : qclass == 1 ? k_score_tiles<0, 24, false> : k_score_tiles<0, 32, false>;
     if (flavor == 2) return qclass == 0 ? k_score_tiles<2, 16, false> : qclass == 1 ? k_score_tiles<2, 24, false> : k_score_tiles<2, 32, false>;
+    if (flavor == 3) return qclass == 0 ? k_score_tiles<3, 16, false> : qclass == 1 ? k_score_tiles<3, 24, false> : k_score_tiles<3, 32, false>;
     return qclass == 0 ? k_score_tiles<1, 16, false> : qclass == 1 ? k_score_tiles<1, 24, false> : k_score_tiles<1, 32, false>;
 }
-size_t tile_smem(bool ov) { return ov ? sizeof(nwap_tile_smem_t<true>) : sizeof(nwap_tile_smem_t<false>); }
+// mode 0: uniform scheme, 1: sparse overrides, 2: dense table
+size_t tile_smem(int mode) { return mode == 1 ? sizeof(nwap_tile_smem_t<1>) : mode == 2 ? sizeof(nwap_tile_smem_t<2>) : sizeof(nwap_tile_smem_t<0>); }
 
 // Device facts, kernel attributes and the memory-pool policy: once per device per process.
 int ensure_device_cache(int device, device_cache **out)
@@ -137,10 +142,10 @@ int ensure_device_cache(int device, device_cache **out)
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
         unsigned long long keep = ~0ull;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-        for (int f = 0; f < 4; ++f)          // f == 3: sparse-override build
+        for (int f = 0; f < 5; ++f)          // f == 3: sparse-override build, f == 4: dense-table build
             for (int w = 0; w < 3; ++w) {
-                tile_kernel_t k = tile_kernel(f == 3 ? 1 : f, w, f == 3);
-                const size_t smem = tile_smem(f == 3);
+                tile_kernel_t k = tile_kernel(f == 3 ? 1 : f == 4 ? 3 : f, w, f == 3);
+                const size_t smem = tile_smem(f == 3 ? 1 : f == 4 ? 2 : 0);
                 CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 int occ = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem));
@@ -225,10 +230,13 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
 {
     if (start >= end) return NWAP_OK;
     const bool fast_ok = (!c->general || c->sparse_ov) && c->qmax <= NWAP_MAXLEN_FAST;
+    const bool tab_ok = c->general && c->tab_ok && c->qmax <= NWAP_MAXLEN_FAST;
     const bool sym_ok = fast_ok && !c->general && nwap_flavor2_ok(c->match, c->mismatch);
     // PACKED3 (2 DPX + IMAD + IADD) is ~8 % faster than PACKED (2 DPX + 2 IMAD) and ~14 % faster than PACKED_SYM
     // (2 DPX + IADD3: one issue fewer, but IADD3 shares the DPX pipe): profiles/r01f_ab_packed_sym.txt
-    if (variant == NWAP_VARIANT_AUTO) variant = fast_ok ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
+    if (variant == NWAP_VARIANT_AUTO) variant = fast_ok ? NWAP_VARIANT_PACKED3 : tab_ok ? NWAP_VARIANT_PACKED_TAB : NWAP_VARIANT_SIMPLE;
+    if (variant == NWAP_VARIANT_PACKED_TAB && !tab_ok)
+        return fail(NWAP_EINVAL, "packed_tab kernel needs a dense similarity table with K <= %d and max word length <= %d", NWAP_OV_MAXK, NWAP_MAXLEN_FAST);
     if (variant == NWAP_VARIANT_PACKED_SYM && !sym_ok)
         return fail(NWAP_EINVAL, "packed_sym kernel needs a uniform scheme with match >= mismatch and max word length <= %d (have %d%s)",
                     NWAP_MAXLEN_FAST, c->qmax, c->general ? ", similarity overrides" : "");
@@ -252,8 +260,9 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
         return NWAP_OK;
     }
 
-    const bool ov = c->general;                       // here: general implies sparse_ov
-    const int flavor = variant == NWAP_VARIANT_PACKED_SYM ? 2 : (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
+    const bool tab = variant == NWAP_VARIANT_PACKED_TAB;
+    const bool ov = c->general && !tab;               // here: general and not tab implies sparse_ov
+    const int flavor = tab ? 3 : variant == NWAP_VARIANT_PACKED_SYM ? 2 : (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
     const int qclass = c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
     nwap_tile_params p;
     p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad;
@@ -263,12 +272,14 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.r_last = nwap_row_of(end - 1, c->n);
     p.c_end = nwap_col_of(end - 1, c->n, p.r_last);
     p.out = out_dev;
-    p.sc = nwap_make_consts(c->match, c->mismatch, c->gap, flavor);
+    p.sc = tab ? nwap_make_consts(c->tab_max, c->tab_max, c->gap, 3) : nwap_make_consts(c->match, c->mismatch, c->gap, flavor);
+    if (tab) p.sc.symmul = (uint32_t)c->K;           // staged row symbol = row offset a*K in the table
     p.stats = c->d_stats; p.want_hist = want_hist;
     p.unit_counter = c->d_counter;
-    p.ov_table = ov ? c->d_ov : nullptr; p.ov_K = ov ? c->K : 0;
+    p.ov_table = ov ? c->d_ov : nullptr; p.ov_K = (ov || tab) ? c->K : 0;
+    p.etab = tab ? c->d_etab : nullptr;
 
-    const int occ = std::max(1, c->occ_tiles[(ov ? 3 : flavor) * 3 + qclass]);
+    const int occ = std::max(1, c->occ_tiles[(ov ? 3 : tab ? 4 : flavor) * 3 + qclass]);
     const int64_t slots = (int64_t)c->sm_count * occ;
     // bands per group: as large as possible (amortises the per-unit sort) while
     // leaving >= 24 units per resident CTA for dynamic balance.
@@ -287,7 +298,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.us = us; p.unit_begin = ubeg; p.unit_count = ucount;
     const int64_t grid = std::min<int64_t>(slots, ucount);
     CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
-    tile_kernel(flavor, qclass, ov)<<<(unsigned)grid, NWAP_THREADS, tile_smem(ov), st>>>(p);
+    tile_kernel(flavor, qclass, ov)<<<(unsigned)grid, NWAP_THREADS, tile_smem(ov ? 1 : tab ? 2 : 0), st>>>(p);
     g_launches++;
     CK(cudaGetLastError());
     return NWAP_OK;
@@ -412,8 +423,19 @@ int nwap_set_similarity(nwap_ctx *c, const int8_t *sim, int K)
         CK(dev_alloc(&c->d_ov, sizeof(nwap_ov_row) * (size_t)K));
         CK(cudaMemcpyAsync(c->d_ov, tab.data(), sizeof(nwap_ov_row) * (size_t)K, cudaMemcpyHostToDevice, 0));
     }
+    // dense but small alphabet: E = M - sim for the packed kernel's table-driven flavour
+    if (c->d_etab) { CK(cudaDeviceSynchronize()); dev_free(c->d_etab); c->d_etab = nullptr; }
+    c->tab_ok = K <= NWAP_OV_MAXK;       // (a sparse table can run either way; `auto` prefers the sparse-override cell)
+    std::vector<uint8_t> etab;
+    if (c->tab_ok) {
+        c->tab_max = mx;
+        etab.resize((size_t)K * K);
+        for (int i = 0; i < K * K; ++i) etab[i] = (uint8_t)(mx - (int)sim[i]);
+        CK(dev_alloc(&c->d_etab, etab.size()));
+        CK(cudaMemcpyAsync(c->d_etab, etab.data(), etab.size(), cudaMemcpyHostToDevice, 0));
+    }
     const int rc = build_sim_table(c, sim);
-    CK(cudaStreamSynchronize(0));        // tab / sim are host temporaries; other streams read the tables
+    CK(cudaStreamSynchronize(0));        // tab / etab / sim are host temporaries; other streams read the tables
     return rc;
 }
 
@@ -422,7 +444,7 @@ void nwap_destroy(nwap_ctx *c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();             // nothing may still be reading the store or writing the slabs
-    dev_free(c->d_ids); dev_free(c->d_lens); dev_free(c->d_sim); dev_free(c->d_stats); dev_free(c->d_ov);
+    dev_free(c->d_ids); dev_free(c->d_lens); dev_free(c->d_sim); dev_free(c->d_stats); dev_free(c->d_ov); dev_free(c->d_etab);
     dev_free(c->d_counter); dev_free(c->d_block_counts); dev_free(c->d_total);
     if (c->pipe) {                       // back to the device cache for the next context
         std::lock_guard<std::mutex> lock(g_cache_mutex);

@@ -72,6 +72,11 @@ NWAP_HD nwap_scheme_consts nwap_make_consts(int match, int mismatch, int gap, in
     c.symmul = 65537u;
     c.t2 = 0u;
     c.c2 = 0u;
+    if (flavor == 3) {
+        // table-driven cell (dense similarity tables): `match` is the table's maximum M; the staged row symbol is
+        // the symbol's row offset a*K in the K x K table of E = M - sim (symmul is set to K by the caller)
+        c.neg_delta = 0u;
+    }
     if (flavor == 2) {
         c.alpha = gap;
         c.u2 = 0u;                                  // every boundary cell H'[i][0] is BIAS
@@ -388,6 +393,45 @@ inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatc
         out[a] = r;
     }
     return true;
+}
+
+// ---- dense similarity tables (FLAVOR 3): sim(a, b) = M - E[a][b] with M the table's maximum and E a K x K
+// uint8 table in shared memory.  With match := M the potentials of FLAVOR 1 carry over and the diagonal term is
+//     dw = diag - (E[a_i][b0_j] | E[a_i][b1_j] << 16)
+// (non-negative halves subtracted from biased halves: no borrow crosses).  Two byte loads per packed cell replace
+// the compare + multiply; c0/c1 hold the lane's column symbols as byte offsets.
+template <int LB>
+NWAP_HD void nwap_dp_row_tab(uint32_t rowoff, const uint32_t *c0, const uint32_t *c1, uint32_t (&P)[LB + 1],
+                             uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc, const uint8_t *etab)
+{
+    const uint8_t *row = etab + rowoff;
+    uint32_t left = left0;
+    uint32_t dw = d0 - ((uint32_t)row[c0[0]] | ((uint32_t)row[c1[0]] << 16));
+#pragma unroll
+    for (int j = 1; j <= LB; ++j) {
+        uint32_t dw_next = 0;
+        if (j < LB) dw_next = P[j] - ((uint32_t)row[c0[j]] | ((uint32_t)row[c1[j]] << 16));
+        const uint32_t cur = nwap_vimax3_s16x2(dw, P[j] + sc.u2, left);
+        P[j] = cur;
+        left = cur;
+        dw = dw_next;
+    }
+}
+
+template <int LB>
+NWAP_HD void nwap_dp_word_tab(const nwap_sym2 *row_sym2, int la, const uint32_t *c0, const uint32_t *c1,
+                              uint32_t (&P)[LB + 1], const nwap_scheme_consts &sc, const uint8_t *etab)
+{
+#pragma unroll
+    for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
+    uint32_t d0 = NWAP_BIAS2;
+    const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
+#pragma unroll 1
+    do {
+        const nwap_sym2 x = *s++;
+        nwap_dp_row_tab<LB>(x.a2, c0, c1, P, d0, x.left0, sc, etab);
+        d0 = x.left0;
+    } while (s != e);
 }
 
 // Whole pair-of-pairs DP for one row word; returns the packed H' values at

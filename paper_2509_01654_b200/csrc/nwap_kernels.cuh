@@ -60,7 +60,8 @@ struct nwap_tile_params {
     nwap_dev_stats *stats;
     int want_hist;
     const nwap_ov_row *ov_table;   // sparse-override mode: (ov_K) rows on the device, else NULL
-    int ov_K;
+    int ov_K;                      // alphabet size K of the override / dense table
+    const uint8_t *etab;           // dense-table mode (FLAVOR 3): K x K table of M - sim on the device, else NULL
 };
 
 struct alignas(16) nwap_row_meta {
@@ -78,15 +79,17 @@ struct alignas(16) nwap_row_meta {
 // shared memory carve-up of k_score_tiles
 // ---------------------------------------------------------------------------
 #define NWAP_OV_MAXK 128               // largest alphabet the sparse-override table holds in shared memory
-template <bool OV> struct nwap_sym_of { typedef nwap_sym2 type; };
-template <> struct nwap_sym_of<true> { typedef nwap_sym4 type; };
+template <int MODE> struct nwap_sym_of { typedef nwap_sym2 type; };
+template <> struct nwap_sym_of<1> { typedef nwap_sym4 type; };
 
-template <bool OV>
+// MODE 0: uniform scheme, 1: sparse overrides (per-symbol correction rows), 2: dense table (K x K bytes of M - sim)
+template <int MODE>
 struct nwap_tile_smem_t {
     alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
-    typedef typename nwap_sym_of<OV>::type sym_t;
+    typedef typename nwap_sym_of<MODE>::type sym_t;
     alignas(16) sym_t rowsym[NWAP_R][NWAP_MAXLEN_FAST + 1];      // {a*65537, H'[i+1][0] (, override row)} per matrix row
-    alignas(16) nwap_ov_row ov[OV ? NWAP_OV_MAXK : 1];              // per-symbol override table (sparse-override mode)
+    alignas(16) nwap_ov_row ov[MODE == 1 ? NWAP_OV_MAXK : 1];       // per-symbol override table (sparse-override mode)
+    alignas(16) uint8_t etab[MODE == 2 ? NWAP_OV_MAXK * NWAP_OV_MAXK : 16];   // dense-table mode
     alignas(16) nwap_row_meta meta[NWAP_R];
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
     uint8_t clen[NWAP_C];         // their lengths
@@ -100,7 +103,7 @@ struct nwap_tile_smem_t {
     int next_chunk;
 };
 
-typedef nwap_tile_smem_t<false> nwap_tile_smem;
+typedef nwap_tile_smem_t<0> nwap_tile_smem;
 
 __device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
 {
@@ -277,6 +280,60 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
     nwap_close_chunk(ls, ca);
 }
 
+
+// Dense-table chunks (FLAVOR 3): per-row dispatch with the shared epilogue; the lane's column symbols are kept
+// as byte offsets (two registers per matrix column) for the table loads of nwap_dp_row_tab.
+template <int LB>
+__device__ __forceinline__ void nwap_row_dp_tab(const nwap_sym2 *sym, int la, const uint32_t *c0, const uint32_t *c1,
+                                                int l0, int l1, const nwap_scheme_consts &sc, const uint8_t *etab,
+                                                uint32_t &v, uint32_t &vm1, uint32_t &vm2, bool deep)
+{
+    uint32_t P[LB + 1];
+    nwap_dp_word_tab<LB>(sym, la, c0, c1, P, sc, etab);
+    v = P[LB];
+    vm1 = P[LB >= 2 ? LB - 1 : LB];
+    vm2 = P[LB >= 3 ? LB - 2 : LB];
+    if (deep) {
+        uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
+#pragma unroll
+        for (int j = 1; j < LB; ++j) {
+            if (j == l0) lo = P[j] & 0xffffu;
+            if (j == l1) hi = P[j] & 0xffff0000u;
+        }
+        v = lo | hi;
+    }
+}
+
+template <int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk_tab(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                   const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                   const nwap_lane_cols &c, int mixmode, bool fast,
+                                                   int want_hist, nwap_lane_stats &ls)
+{
+    uint32_t c0[QMAX], c1[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) { c0[j] = nwap_byte_of(w0, j); c1[j] = nwap_byte_of(w1, j); }
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+    const bool deep = mixmode > 2;
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;
+        const nwap_sym2 *sym = reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]);
+        uint32_t v = 0, vm1 = 0, vm2 = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_row_dp_tab<(n <= QMAX ? n : 1)>(sym, la, c0, c1, c.l0, c.l1, sc, sm.etab, v, vm1, vm2, deep); \
+        break;
+        switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+    nwap_close_chunk(ls, ca);
+}
+
 // NWAP_HOIST=1 (default): the length dispatch is done once per chunk and each length body owns the
 // whole row loop with the emit inlined.  With 4-warp CTAs this lost 13-18 % to instruction-cache
 // misses (profiles/r01e); with 10-warp CTAs it gains 3-4 % (profiles/r01h_ab_big_cta.txt).
@@ -363,11 +420,11 @@ __device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_
 // QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
 // accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
 template <int FLAVOR, int QMAX, bool OV>
-__global__ void __launch_bounds__(NWAP_THREADS, ((OV && QMAX > 24) ? 1 : NWAP_MINB))   // the 32-wide sparse-override build needs > 96 registers
+__global__ void __launch_bounds__(NWAP_THREADS, (((OV || FLAVOR == 3) && QMAX > 24) ? 1 : NWAP_MINB))   // the 32-wide sparse-override / table builds need > 96 registers
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    typedef nwap_tile_smem_t<OV> smem_t;
+    typedef nwap_tile_smem_t<(OV ? 1 : (FLAVOR == 3 ? 2 : 0))> smem_t;
     smem_t &sm = *reinterpret_cast<smem_t *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const nwap_scheme_consts sc = p.sc;
@@ -376,6 +433,9 @@ k_score_tiles(const nwap_tile_params p)
 
     if (tid == 0) { sm.sum = 0; sm.count = 0; sm.mn = 127; sm.mx = -128; }
     for (int b = tid; b < 256; b += NWAP_THREADS) sm.hist[b] = 0;
+    if (FLAVOR == 3) {
+        for (int w = tid; w < p.ov_K * p.ov_K; w += NWAP_THREADS) sm.etab[w] = p.etab[w];
+    }
     if (OV) {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(p.ov_table);
         uint32_t *dst = reinterpret_cast<uint32_t *>(sm.ov);
@@ -530,6 +590,10 @@ k_score_tiles(const nwap_tile_params p)
                 const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
                 const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
                 const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
+                if (FLAVOR == 3) {
+                    nwap_run_chunk_tab<QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+                    continue;
+                }
 #if NWAP_HOIST
                 // two code families only where the register budget allows (the 32-wide and sparse-override
                 // instantiations would spill): there the hoisted bodies also carry the slow emit

@@ -60,7 +60,52 @@ static uint32_t run_pair_ov(const uint8_t *a, int la, const uint8_t *b0, int lb0
     return lo | (hi << 16);
 }
 
+template <int LB>
+static uint32_t run_pair_tab(const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,
+                             const nwap_scheme_consts &sc, const uint8_t *etab, int K)
+{
+    nwap_sym2 row2[256];
+    for (int i = 0; i < la; ++i) {
+        row2[i].a2 = (uint32_t)a[i] * (uint32_t)K;
+        row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+    }
+    uint32_t c0[LB], c1[LB];
+    for (int j = 0; j < LB; ++j) { c0[j] = j < lb0 ? b0[j] : 0u; c1[j] = j < lb1 ? b1[j] : 0u; }
+    uint32_t P[LB + 1];
+    nwap_dp_word_tab<LB>(row2, la, c0, c1, P, sc, etab);
+    uint32_t lo = 0, hi = 0;
+    for (int j = 1; j <= LB; ++j) {
+        if (j == lb0) lo = P[j] & 0xffffu;
+        if (j == lb1) hi = P[j] >> 16;
+    }
+    return lo | (hi << 16);
+}
+
 extern "C" {
+
+// Dense-table mode: sim is a K x K int8 table; E = max - sim.
+int emul_pair_scores_tab(int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,
+                         const int8_t *sim, int K, int gap, int *s0, int *s1)
+{
+    if (LB < 1 || LB > 32 || lb0 > LB || lb1 > LB || la < 1 || K > 128) return -1;
+    static uint8_t etab[128 * 128];
+    int M = -128;
+    for (int i = 0; i < K * K; ++i) M = sim[i] > M ? sim[i] : M;
+    for (int i = 0; i < K * K; ++i) etab[i] = (uint8_t)(M - sim[i]);
+    nwap_scheme_consts sc = nwap_make_consts(M, M, gap, 3);
+    uint32_t v = 0;
+    switch (LB) {
+#define CASE(n) case n: v = run_pair_tab<n>(a, la, b0, lb0, b1, lb1, sc, etab, K); break;
+        CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+        CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+        CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24)
+        CASE(25) CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
+#undef CASE
+    }
+    *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
+    *s1 = nwap_unbias(v >> 16, la, lb1, sc);
+    return 0;
+}
 
 // Sparse-override mode: sim is a dense K x K int8 table; returns -2 when it is not sparse enough.
 int emul_pair_scores_ov(int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,

@@ -370,6 +370,54 @@ def test_sparse_override_schemes_on_the_packed_kernel():
             ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed3")
 
 
+def test_dense_similarity_tables_on_the_packed_kernel():
+    """Dense override tables (every pair has its own value) with K <= 128 run on the packed kernel's table-driven
+    flavour: same bytes and statistics as the generic kernel and the oracle; K > 128 falls back to the generic one."""
+    rng = np.random.default_rng(314)
+    for trial, (K, q, n) in enumerate([(6, 8, 300), (40, 24, 2500), (128, 16, 1200), (17, 32, 700), (3, 1, 50), (40, 12, 5200)]):
+        while True:
+            g = int(rng.integers(-4, 1))
+            lo_s, hi_s = sorted(int(x) for x in rng.integers(-4, 5, size=2))
+            if min(0, 2 * q * g, q * lo_s) >= -128 and max(0, 2 * q * g, q * hi_s) <= 127 and lo_s < hi_s:
+                break
+        ov = {(a, b): int(rng.integers(lo_s, hi_s + 1)) for a in range(K) for b in range(a, K)}
+        lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
+        lens[0] = q
+        ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
+        ids[1, 0] = K - 1
+        scheme = nw.ScoringScheme(ov[(0, 0)], ov[(0, 1)] if K > 1 else 0, g, overrides=ov)
+        P = nw.num_edges(n)
+        ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P, threads=8)
+        with NwapContext(ids, lens, scheme) as ctx:
+            for v in ("auto", "packed_tab", "simple"):
+                got, st = _score(ctx, 0, P, v, want_hist=(trial % 2 == 0), offset=trial)
+                assert np.array_equal(got, ref), (trial, v, K, q, g)
+                assert st[:4] == (rsum, rmin, rmax, P)
+            s, e = P // 3, P // 3 + min(P // 2, 70_001)
+            got, st = _score(ctx, s, e, "packed_tab", offset=3)
+            assert np.array_equal(got, ref[s:e])
+            if K >= 17:          # certainly more than 3 override partners per symbol: the compare-based cells refuse
+                with pytest.raises(ValueError, match="packed kernel"):
+                    ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed3")
+    # a uniform scheme has no table: packed_tab is refused
+    with NwapContext(ids, lens, nw.ScoringScheme(1, -1, -1)) as ctx:
+        with pytest.raises(ValueError, match="packed_tab"):
+            ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed_tab")
+    # K > 128: generic kernel
+    K, n, q = 200, 150, 6
+    ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
+    ids[0, 0] = K - 1
+    lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
+    ov = {(a, b): int((a * 7 + b * 3) % 5 - 2) for a in range(K) for b in range(a, K)}
+    scheme = nw.ScoringScheme(1, -1, -2, overrides=ov)
+    ref, *_ = _oracle(ids, lens, scheme, 0, nw.num_edges(n))
+    with NwapContext(ids, lens, scheme) as ctx:
+        got, _ = _score(ctx, 0, nw.num_edges(n), "auto")
+        assert np.array_equal(got, ref)
+        with pytest.raises(ValueError, match="packed_tab"):
+            ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed_tab")
+
+
 # ---- BASELINE.json configs -------------------------------------------------------------------
 
 def test_c1_full_config_through_entry_point(golden_samples):
