@@ -87,10 +87,10 @@ int nwap_create(nwap_ctx **ctx_out, int device,
 
 /* ScoringScheme.overrides (aligner.py:51-65, engine.py:113-116): install a
  * dense symmetric K x K similarity table (host int8, row-major).  Symbols >= K
- * are rejected.  If the table is the uniform scheme plus at most 3 overrides per symbol
- * (and K <= 128) the packed kernel still runs it (sparse-override mode); a denser table with
- * K <= 128 runs on the packed kernel's table-driven flavour (NWAP_VARIANT_PACKED_TAB);
- * anything else is routed through the generic one-thread-per-pair kernel. */
+ * are rejected.  With K <= 128 the packed tile kernel runs the table through its table-driven
+ * flavour (NWAP_VARIANT_PACKED_TAB, what NWAP_VARIANT_AUTO picks); a table that is the uniform
+ * scheme plus at most 3 overrides per symbol can also run as corrections of the compare-based
+ * cell (NWAP_VARIANT_PACKED3); anything else goes to the generic one-thread-per-pair kernel. */
 int nwap_set_similarity(nwap_ctx *ctx, const int8_t *sim, int K);
 
 void nwap_destroy(nwap_ctx *ctx);
