@@ -234,7 +234,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     const bool sym_ok = fast_ok && !c->general && nwap_flavor2_ok(c->match, c->mismatch);
     // PACKED3 (2 DPX + IMAD + IADD) is ~8 % faster than PACKED (2 DPX + 2 IMAD) and ~14 % faster than PACKED_SYM
     // (2 DPX + IADD3: one issue fewer, but IADD3 shares the DPX pipe): profiles/r01f_ab_packed_sym.txt
-    // override tables: the table-driven cell (4.2 TCUPS) beats the sparse-correction cell (2.7 TCUPS with six overridden
+    // override tables: the table-driven cell (4.8 TCUPS) beats the sparse-correction cell (2.7 TCUPS with six overridden
     // pairs, profiles/r01_ov_bench.txt) whenever the alphabet fits shared memory, so `auto` takes it first
     if (variant == NWAP_VARIANT_AUTO)
         variant = tab_ok ? NWAP_VARIANT_PACKED_TAB : fast_ok ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;

@@ -304,6 +304,26 @@ __device__ __forceinline__ void nwap_row_dp_tab(const nwap_sym2 *sym, int la, co
     }
 }
 
+// one length dispatch per chunk; the body owns the loop over the band's rows (as the hoisted uniform-scheme bodies)
+template <int LB, class SM>
+__device__ __forceinline__ void nwap_chunk_rows_tab(SM &sm, const nwap_scheme_consts &sc, const uint32_t *c0,
+                                                    const uint32_t *c1, const nwap_lane_cols &c, int mixmode, bool fast,
+                                                    int want_hist, nwap_lane_stats &ls, nwap_chunk_acc &ca)
+{
+    const bool deep = mixmode > 2;
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;
+        uint32_t v, vm1, vm2;
+        nwap_row_dp_tab<LB>(reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]), la, c0, c1, c.l0, c.l1, sc, sm.etab,
+                            v, vm1, vm2, deep);
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+}
+
 template <int QMAX, int QW, class SM>
 __device__ __forceinline__ void nwap_run_chunk_tab(int LB, SM &sm, const nwap_scheme_consts &sc,
                                                    const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
@@ -314,23 +334,12 @@ __device__ __forceinline__ void nwap_run_chunk_tab(int LB, SM &sm, const nwap_sc
 #pragma unroll
     for (int j = 0; j < QMAX; ++j) { c0[j] = nwap_byte_of(w0, j); c1[j] = nwap_byte_of(w1, j); }
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
-    const bool deep = mixmode > 2;
-#pragma unroll 1
-    for (int rr = 0; rr < NWAP_R; ++rr) {
-        const nwap_row_meta &m = sm.meta[rr];
-        const int la = m.la;
-        if (la == 0) continue;
-        const nwap_sym2 *sym = reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]);
-        uint32_t v = 0, vm1 = 0, vm2 = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
-        if (n <= QMAX) nwap_row_dp_tab<(n <= QMAX ? n : 1)>(sym, la, c0, c1, c.l0, c.l1, sc, sm.etab, v, vm1, vm2, deep); \
+        if (n <= QMAX) nwap_chunk_rows_tab<(n <= QMAX ? n : 1)>(sm, sc, c0, c1, c, mixmode, fast, want_hist, ls, ca); \
         break;
-        switch (LB) { NWAP_CASES_1_32 default: break; }
+    switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
-        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
-        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
-    }
     nwap_close_chunk(ls, ca);
 }
 
