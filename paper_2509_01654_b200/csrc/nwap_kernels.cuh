@@ -761,7 +761,9 @@ __global__ void k_init_stats(nwap_dev_stats *s, unsigned long long *counter)
     if (t == 0) { s->sum = 0; s->count = 0; s->mn = 127; s->mx = -128; if (counter) *counter = 0; }
 }
 
-// Dense payload -> statistics (HBM-bound: 1 byte read per edge).
+// Dense payload -> statistics (HBM-bound: 1 byte read per edge).  The loop only feeds the 256-bin histogram
+// (one shared-memory atomic per edge); sum, minimum and maximum are derived from the CTA's histogram at the end
+// (thread t owns bin t, value t - 128), so the per-edge work is an extract and an atomic.
 __global__ void __launch_bounds__(256)
 k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stats *stats)
 {
@@ -772,8 +774,6 @@ k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stat
     shist[tid] = 0;
     if (tid == 0) { ssum = 0; smn = 127; smx = -128; }
     __syncthreads();
-    long long tsum = 0;
-    int tmn = 127, tmx = -128;
     // head bytes until 16-byte alignment, vector body, tail
     const uintptr_t addr = reinterpret_cast<uintptr_t>(payload);
     int64_t head = (int64_t)((16 - (addr & 15)) & 15);
@@ -781,25 +781,34 @@ k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stat
     const int64_t nvec = (count - head) >> 4;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
     const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-    auto one = [&](int s) {
-        tsum += s; tmn = min(tmn, s); tmx = max(tmx, s);
-        atomicAdd(&shist[s + 128], 1u);
-    };
-    if (gtid < head) one((int)payload[gtid]);
+    if (gtid < head) atomicAdd(&shist[(int)payload[gtid] + 128], 1u);
     const uint4 *p4 = reinterpret_cast<const uint4 *>(payload + head);
     for (int64_t v = gtid; v < nvec; v += gstride) {
         const uint4 x = p4[v];
-        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        const uint32_t w[4] = {x.x ^ 0x80808080u, x.y ^ 0x80808080u, x.z ^ 0x80808080u, x.w ^ 0x80808080u};   // bin = score + 128
 #pragma unroll
-        for (int k = 0; k < 16; ++k) one((int)(int8_t)((w[k >> 2] >> (8 * (k & 3))) & 0xffu));
+        for (int k = 0; k < 16; ++k) atomicAdd(&shist[(w[k >> 2] >> (8 * (k & 3))) & 0xffu], 1u);
     }
     const int64_t tail0 = head + (nvec << 4);
-    if (tail0 + gtid < count) one((int)payload[tail0 + gtid]);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&ssum), (unsigned long long)tsum);
-    atomicMin(&smn, tmn);
-    atomicMax(&smx, tmx);
+    if (tail0 + gtid < count) atomicAdd(&shist[(int)payload[tail0 + gtid] + 128], 1u);
     __syncthreads();
-    if (shist[tid]) atomicAdd(&stats->hist[tid], (unsigned long long)shist[tid]);
+    // thread t: bin t
+    const unsigned int h = shist[tid];
+    long long part = (long long)h * (long long)(tid - 128);
+    int mn = h ? tid - 128 : 127, mx = h ? tid - 128 : -128;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        part += __shfl_xor_sync(0xffffffffu, part, o);
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((tid & 31) == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&ssum), (unsigned long long)part);
+        atomicMin(&smn, mn);
+        atomicMax(&smx, mx);
+    }
+    if (h) atomicAdd(&stats->hist[tid], (unsigned long long)h);
+    __syncthreads();
     if (tid == 0) {
         atomicAdd(reinterpret_cast<unsigned long long *>(&stats->sum), (unsigned long long)ssum);
         atomicMin(&stats->mn, smn);
