@@ -648,7 +648,7 @@ int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, in
 {
     if (!c) return fail(NWAP_EINVAL, "null context");
     nwap_keep_params kp;
-    kp.threshold = threshold; memset(kp.smin, 0, sizeof kp.smin); memset(kp.smax, 0, sizeof kp.smax); kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    kp.threshold = threshold; memset(kp.smin, 0, sizeof kp.smin); memset(kp.smax, 0, sizeof kp.smax); kp.gmin = 0; kp.gmax = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
     return compact_common(c, payload_dev, start, end, 0, kp, idx_out_dev, score_out_dev, cap, count_host, degree_dev,
                           (cudaStream_t)stream);
 }
@@ -678,7 +678,7 @@ int nwap_hist_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, 
     CK(cudaSetDevice(c->device));
     cudaStream_t st = (cudaStream_t)stream;
     nwap_keep_params kp;
-    kp.threshold = 0; memset(kp.smin, 0, sizeof kp.smin); memset(kp.smax, 0, sizeof kp.smax); kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    kp.threshold = 0; memset(kp.smin, 0, sizeof kp.smin); memset(kp.smax, 0, sizeof kp.smax); kp.gmin = 0; kp.gmax = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
     const size_t smem = sizeof(unsigned int) * NWAP_NHIST_SPAN;
     CK(cudaFuncSetAttribute(k_hist_normalized, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t runs = (count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;

@@ -842,6 +842,7 @@ struct nwap_keep_params {
     // reference's IEEE-double expression (graph.py:96-98) for all 256 x 255 (s, m), so the device test is
     // two integer compares and exactly the reference's keep-mask; an empty interval is smin > smax.
     int8_t smin[256], smax[256];
+    int gmin, gmax;          // MODE 1: loosest bounds over all lengths (gmin > gmax: nothing can be kept)
 };
 
 // host side of the table above
@@ -857,6 +858,9 @@ inline void nwap_fill_norm_bounds(nwap_keep_params &kp, double lo, double hi)
         kp.smin[m] = (int8_t)first;
         kp.smax[m] = (int8_t)last;
     }
+    kp.gmin = 127; kp.gmax = -128;
+    for (int m = 1; m < 256; ++m)
+        if (kp.smin[m] <= kp.smax[m]) { kp.gmin = kp.gmin < kp.smin[m] ? kp.gmin : kp.smin[m]; kp.gmax = kp.gmax > kp.smax[m] ? kp.gmax : kp.smax[m]; }
 }
 
 // The payload slice is scanned through its 16-byte ALIGNED window: window byte w holds edge
@@ -939,6 +943,35 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
     }
     // MODE 1: lo <= 100.0*score/max(len_r, len_c) <= hi (graph.py:96-98) through the per-length score
     // bounds in shared memory; (r, c) walks the triangle
+    // candidates first, from the payload alone: a score outside [gmin, gmax] (the loosest bounds over all lengths)
+    // cannot be kept whatever the word lengths are.  Selective filters reject most edges here, 4 per SWAR step,
+    // before any index recovery or length fetch.
+    if (kp.gmin > kp.gmax) return 0;
+    unsigned long long cand = 0;
+    {
+        const uint32_t Tlo = (uint32_t)(kp.gmin + 128);                 // gmin >= -128
+        const uint32_t lo_rep = (Tlo & 0x7fu) * 0x01010101u;
+        const bool lo_th = (Tlo & 0x80u) != 0;
+        const bool all_lo = kp.gmin <= -128;
+        const bool has_hi = kp.gmax < 127;
+        const uint32_t Thi = (uint32_t)(kp.gmax + 1 + 128);              // scores >= gmax + 1 are out
+        const uint32_t hi_rep = (Thi & 0x7fu) * 0x01010101u;
+        const bool hi_th = (Thi & 0x80u) != 0;
+#pragma unroll
+        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+            const uint32_t w[4] = {vec[v].x, vec[v].y, vec[v].z, vec[v].w};
+            unsigned b16 = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                unsigned ok = all_lo ? 0xfu : nwap_ge_bits4(w[q], lo_rep, lo_th);
+                if (has_hi) ok &= ~nwap_ge_bits4(w[q], hi_rep, hi_th);
+                b16 |= ok << (4 * q);
+            }
+            cand |= (unsigned long long)b16 << (16 * v);
+        }
+        cand &= valid;
+    }
+    if (cand == 0) return 0;
     const int64_t kb = max(k_first, (int64_t)0);
     int64_t r = nwap_row_of(kp.start + kb, kp.n);
     int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
@@ -953,10 +986,12 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
                 const int e = 16 * v + j;
-                const int sc = (int)(int8_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
-                const int lc = (int)((L[e >> 2] >> (8 * (e & 3))) & 0xffu);
-                const short2 b = bounds[max(lr, lc)];
-                if (sc >= (int)b.x && sc <= (int)b.y) bits |= 1ull << e;
+                if ((cand >> e) & 1ull) {
+                    const int sc = (int)(int8_t)((w[j >> 2] >> (8 * (j & 3))) & 0xffu);
+                    const int lc = (int)((L[e >> 2] >> (8 * (e & 3))) & 0xffu);
+                    const short2 b = bounds[max(lr, lc)];
+                    if (sc >= (int)b.x && sc <= (int)b.y) bits |= 1ull << e;
+                }
             }
         }
         return bits;
