@@ -1,6 +1,7 @@
 """Parity of the CUDA path (through the C ABI) with the oracle, the reference's golden
 vectors and the reference tests' own cases.  Bit-exact: this is integer/byte work."""
 import hashlib
+import json
 
 import numpy as np
 import pytest
@@ -451,6 +452,10 @@ def test_c2_every_byte_against_oracle(golden_samples):
         host = torch.empty(P, dtype=torch.int8).pin_memory()
         st = ctx.score_range_host(0, P, host, want_hist=True)
         assert np.array_equal(host.numpy(), ref) and st[:4] == (rsum, rmin, rmax, P)
+        # ... and the payload the UNMODIFIED reference engine produced for this config (its digest and ComputeStats)
+        gold = json.loads((GOLDEN / "c2_reference_digest.json").read_text())
+        assert hashlib.blake2b(host.numpy().tobytes(), digest_size=16).hexdigest() == gold["payload_blake2b_128"]
+        assert (st[1], st[2], st[0] / P) == (gold["min"], gold["max"], gold["mean"])
         ps = ctx.payload_stats(out)
         assert ps[:4] == (rsum, rmin, rmax, P) and np.array_equal(ps[4], orc.np_histogram(ref))
         # equal-work shards written independently reproduce the payload (multi-GPU path, one GPU)

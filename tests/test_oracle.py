@@ -197,3 +197,26 @@ def test_consumer_oracles_match_reference(golden_cases):
             rows = orc.np_rows_of(idx, n)
             cols = orc.np_cols_of(idx, n, rows)
             assert np.array_equal(np.stack([rows, cols], 1), g[f"filter{k}_edges"].astype(np.int64))
+
+
+def test_oracle_reproduces_the_reference_c2_payload():
+    """configs[1] at full size: the C oracle's 199,990,000 bytes hash to the digest of the payload the UNMODIFIED
+    reference engine produced (tests/golden/c2_reference_digest.json, made by make_golden_c2_digest.py), and the
+    statistics equal its ComputeStats."""
+    import hashlib
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_2509_01654_b200 import synth
+
+    gold = json.loads((GOLDEN / "c2_reference_digest.json").read_text())
+    ids, lens, sch = synth.config_store("C2")
+    assert synth.store_digest(ids, lens) == gold["store_digest"] and list(sch) == gold["scheme"]
+    n = len(lens)
+    P = n * (n - 1) // 2
+    sim = orc.similarity_matrix(sch[0], sch[1], int(ids.max()) + 1)
+    payload, ssum, smin, smax = orc.c_score_range(ids.astype(np.int32), lens.astype(np.int32), sim, sch[2], n, 0, P,
+                                                  threads=len(os.sched_getaffinity(0)))
+    assert payload.size == gold["edges"] == P
+    assert hashlib.blake2b(payload.tobytes(), digest_size=16).hexdigest() == gold["payload_blake2b_128"]
+    assert (smin, smax) == (gold["min"], gold["max"]) and ssum / P == gold["mean"]
