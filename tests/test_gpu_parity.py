@@ -490,6 +490,38 @@ def test_sampled_ranges_of_big_configs(golden_samples, cfg):
         assert ctx.cells_in_range(0, ctx.num_edges) == m["total_cells"]
 
 
+def test_c3_every_byte_against_the_reference_itself():
+    """configs[2] at full size: the 8 equal-work shards, scored independently (what 8 ranks would write), hash to the
+    per-shard digests of the payload the UNMODIFIED reference engine produced for the same 100,000 words
+    (tests/golden/c3_reference_digest.json, 4,999,950,000 bytes), their concatenation to its whole-payload digest,
+    and the fused statistics equal its ComputeStats."""
+    from concurrent.futures import ThreadPoolExecutor
+    gold = json.loads((GOLDEN / "c3_reference_digest.json").read_text())
+    ids, lens, sch = synth.config_store("C3")
+    assert synth.store_digest(ids, lens) == gold["store_digest"] and list(sch) == gold["scheme"]
+    P = nw.num_edges(len(lens))
+    assert P == gold["edges"]
+    with NwapContext(ids, lens, nw.ScoringScheme(*sch)) as ctx:
+        bounds = [int(b) for b in ctx.equal_work_bounds(8)]
+        assert bounds == gold["shard_bounds"]
+        host = torch.empty(P, dtype=torch.int8).pin_memory()
+        tot, mn, mx = 0, 127, -128
+        for g in range(8):
+            st = ctx.score_range_host(bounds[g], bounds[g + 1], host[bounds[g]: bounds[g + 1]])
+            assert st[3] == bounds[g + 1] - bounds[g]
+            tot, mn, mx = tot + st[0], min(mn, st[1]), max(mx, st[2])
+    view = memoryview(host.numpy()).cast("B")
+
+    def digest(rng):
+        return hashlib.blake2b(view[rng[0]: rng[1]], digest_size=16).hexdigest()
+
+    with ThreadPoolExecutor(9) as ex:          # hashlib releases the GIL
+        got = list(ex.map(digest, [(bounds[g], bounds[g + 1]) for g in range(8)] + [(0, P)]))
+    assert got[:8] == gold["shard_blake2b_128"]
+    assert got[8] == gold["payload_blake2b_128"]
+    assert (mn, mx, tot / P) == (gold["min"], gold["max"], gold["mean"])
+
+
 def test_c3_two_independent_kernels_agree():
     """configs[2] at full size (4,999,950,000 pairs): the packed DPX kernel and the int32
     one-thread-per-pair kernel must produce the same histogram / sum / min / max, and the same
