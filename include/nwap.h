@@ -40,10 +40,12 @@ extern "C" {
 #define NWAP_ECAPACITY  -5   /* compaction output buffer too small */
 
 /* kernel variants selectable per call (nwap_score_range `variant`) */
-#define NWAP_VARIANT_AUTO    0  /* packed DPX tile kernel when the scheme/store allow it, else simple */
+#define NWAP_VARIANT_AUTO    0  /* packed DPX tile kernel when the scheme/store allow it, else simple; a uniform scheme
+                                 * always allows it: words of 33..64 symbols (gap -1, engine.py:83-90) run the wide build */
 #define NWAP_VARIANT_SIMPLE  1  /* one thread per pair, int32 cells, K x K table: any scheme, any q <= 255 */
 #define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 DPX + 2 IMAD per packed cell */
-#define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 2 DPX + 1 IMAD + 1 IADD per packed cell */
+#define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 2 DPX + 1 IMAD + 1 IADD per packed cell; word length <= 64
+                                 * (chunks longer than 24 symbols are scored block-wise, 16 columns at a time) */
 #define NWAP_VARIANT_PACKED_TAB 5 /* s16x2 DPX tile kernel with a K x K similarity table in shared memory (K <= 128):
                                    * dense override tables; 2 byte loads per packed cell instead of compare + multiply */
 #define NWAP_VARIANT_PACKED_SYM 4 /* s16x2 DPX tile kernel, symmetric gap potential: 2 DPX + 1 IADD3 per packed cell
@@ -149,6 +151,27 @@ int nwap_payload_stats(nwap_ctx *ctx, const int8_t *payload_dev, int64_t count,
 int nwap_compact_range(nwap_ctx *ctx, const int8_t *payload_dev, int64_t start, int64_t end,
                        int threshold, int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap,
                        int64_t *count_host, int32_t *degree_dev, void *stream);
+
+/* The edge writer with score-threshold compaction fused in (BASELINE north_star, kernel K4; keep-mask of
+ * graph.py:91-101 applied where the scores are produced): scores [start, end) exactly as nwap_score_range and
+ * returns the kept edges -- raw score >= threshold -- in increasing linear index in idx_out_dev (int64) /
+ * score_out_dev (int8), *count_host = number kept.  The dense payload is OPTIONAL: with out_dev == NULL no
+ * per-edge byte is written to memory at all, so a 600,000-word job (1.8e11 edges) needs no 180 GB buffer and
+ * runs on one GPU in one call.  The tile kernel appends kept edges as unordered 64-bit keys; a radix sort
+ * restores index order, so the result is identical to nwap_compact_range over the dense payload.
+ * degree_dev as for nwap_compact_range (not zeroed here); stats_host (may be NULL) receives the range's
+ * sum/min/max/count.  More than `cap` (< 2^31) kept edges: NWAP_ECAPACITY, *count_host is the true count and
+ * the output arrays are unspecified.  idx_out_dev doubles as sort scratch.  variant: AUTO or PACKED3, uniform
+ * schemes only.  Synchronises `stream`. */
+int nwap_score_range_compact(nwap_ctx *ctx, int64_t start, int64_t end, int8_t *out_dev, int threshold,
+                             int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
+                             int32_t *degree_dev, nwap_stats *stats_host, int variant, void *stream);
+
+/* The same with the normalised-weight predicate of graph.py:96-98 (lo <= 100.0*score/max(len_r,len_c) <= hi in
+ * IEEE double, as nwap_filter_normalized). */
+int nwap_score_range_filter_normalized(nwap_ctx *ctx, int64_t start, int64_t end, int8_t *out_dev, double lo, double hi,
+                                       int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
+                                       int32_t *degree_dev, nwap_stats *stats_host, int variant, void *stream);
 
 /* graph.py:91-101 filter_view keep-mask on the device: keep the edges of an already scored
  * slice whose NORMALISED weight w = 100.0 * score / max(len_r, len_c) satisfies

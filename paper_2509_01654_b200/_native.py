@@ -30,7 +30,7 @@ EXPORTS = [
     "nwap_set_similarity", "nwap_destroy", "nwap_num_words", "nwap_num_edges", "nwap_max_len",
     "nwap_cells_in_range", "nwap_score_range", "nwap_score_range_host", "nwap_score_range_host_begin",
     "nwap_score_range_host_wait", "nwap_trim", "nwap_read_stats",
-    "nwap_payload_stats", "nwap_compact_range", "nwap_filter_normalized", "nwap_hist_normalized",
+    "nwap_payload_stats", "nwap_compact_range", "nwap_score_range_compact", "nwap_score_range_filter_normalized", "nwap_filter_normalized", "nwap_hist_normalized",
     "nwap_equal_work_bounds", "nwap_rows_cols",
     "nwap_probe", "nwap_launch_count",
 ]
@@ -90,6 +90,8 @@ def lib() -> ctypes.CDLL:
         "nwap_read_stats": (i32, [p, p, p]),
         "nwap_payload_stats": (i32, [p, p, i64, p, p]),
         "nwap_compact_range": (i32, [p, p, i64, i64, i32, p, p, i64, p, p, p]),
+        "nwap_score_range_compact": (i32, [p, i64, i64, p, i32, p, p, i64, p, p, p, i32, p]),
+        "nwap_score_range_filter_normalized": (i32, [p, i64, i64, p, ctypes.c_double, ctypes.c_double, p, p, i64, p, p, p, i32, p]),
         "nwap_filter_normalized": (i32, [p, p, i64, i64, ctypes.c_double, ctypes.c_double, p, p, i64, p, p, p]),
         "nwap_hist_normalized": (i32, [p, p, i64, i64, p, p]),
         "nwap_equal_work_bounds": (i32, [p, i32, p]),

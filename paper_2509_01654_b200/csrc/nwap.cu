@@ -41,10 +41,54 @@ int fail(int code, const char *fmt, ...)
             return fail(NWAP_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
     } while (0)
 
+// Every entry point works on its context's GPU and puts the caller's current device back on return: a host
+// process that also drives torch (or other contexts) must not find its current device changed behind its back.
+struct device_guard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit device_guard(int dev)
+    {
+        int cur = -1;
+        err = cudaGetDevice(&cur);
+        if (err == cudaSuccess && cur != dev) {
+            err = cudaSetDevice(dev);
+            if (err == cudaSuccess) prev = cur;
+        }
+    }
+    ~device_guard() { if (prev >= 0) cudaSetDevice(prev); }
+    device_guard(const device_guard &) = delete;
+    device_guard &operator=(const device_guard &) = delete;
+};
+#define ON_DEVICE(dev) device_guard guard_(dev); CK(guard_.err)
+
 static_assert(sizeof(nwap_dev_stats) == sizeof(nwap_stats), "stats layouts must agree");
 static_assert(sizeof(nwap_tile_smem_t<1>) <= 227 * 1024 && sizeof(nwap_tile_smem_t<2>) <= 227 * 1024, "tile shared memory too large");
+static_assert(2 * sizeof(nwap_tile_smem_t<0, NWAP_MAXLEN_WIDE>) <= 226 * 1024, "the wide build must keep two CTAs per SM");
 
 }  // namespace
+
+nwap_tile_kernel_t nwap_tile_kernel(int family, int qclass)
+{
+    switch (family) {
+    case 0: case 2: return nwap_tiles_f0f2(family, qclass);
+    case 3: return nwap_tiles_ov(qclass);
+    case 4: return nwap_tiles_tab(qclass);
+    case 5: return nwap_tiles_wide(false);
+    case 6: return nwap_tiles_cmp(qclass);
+    case 7: return nwap_tiles_wide(true);
+    default: return nwap_tiles_f1(qclass);
+    }
+}
+
+size_t nwap_tile_smem_bytes(int family)
+{
+    switch (family) {
+    case 3: return sizeof(nwap_tile_smem_t<1>);
+    case 4: return sizeof(nwap_tile_smem_t<2>);
+    case 5: case 7: return sizeof(nwap_tile_smem_t<0, NWAP_MAXLEN_WIDE>);
+    default: return sizeof(nwap_tile_smem_t<0>);
+    }
+}
 
 struct nwap_ctx {
     int device = 0;
@@ -74,7 +118,14 @@ struct nwap_ctx {
     // host-destination pipeline: borrowed from the per-device cache on first use, returned in nwap_destroy
     struct nwap_pipe *pipe = nullptr;
     bool host_pending = false;          // nwap_score_range_host_begin issued, nwap_score_range_host_wait not yet
-    int occ_tiles[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};    // resident CTAs/SM per (flavor 0..2 | ov=3 | table=4, qclass) instantiation
+    int occ_tiles[NWAP_TILE_FAMILIES * 3] = {0};    // resident CTAs/SM per (family, qclass) instantiation (nwap_tile_kernel)
+    // sparse-output mode: key scratch (second sort buffer), digit table, kept counter, per-length bounds
+    unsigned long long *d_keys = nullptr;
+    int64_t keys_cap = 0;
+    unsigned int *d_sort_table = nullptr;
+    int64_t sort_table_cap = 0;
+    unsigned long long *d_kept = nullptr;
+    short2 *d_kbounds = nullptr;
 };
 
 // Two device slabs, two streams and four events: everything nwap_score_range_host needs to overlap
@@ -88,8 +139,6 @@ struct nwap_pipe {
 
 namespace {
 
-typedef void (*tile_kernel_t)(const nwap_tile_params);
-
 // Per-device facts and scratch that outlive a context.  Creating and destroying a context per
 // call (what the reference-shaped entry point does) must not pay cudaGetDeviceProperties, twelve
 // occupancy queries, two 256 MB cudaMalloc/cudaFree pairs and stream/event creation every time:
@@ -97,7 +146,7 @@ typedef void (*tile_kernel_t)(const nwap_tile_params);
 struct device_cache {
     bool ready = false;
     int sm_count = 0;
-    int occ_tiles[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    int occ_tiles[NWAP_TILE_FAMILIES * 3] = {0};
     std::vector<nwap_pipe *> free_pipes;
 };
 std::mutex g_cache_mutex;
@@ -116,18 +165,6 @@ void destroy_pipe(nwap_pipe *p)
     delete p;
 }
 
-// qclass: 0 -> rows up to 16 symbols, 1 -> up to 24, 2 -> up to 32; ov: sparse-override build
-tile_kernel_t tile_kernel(int flavor, int qclass, bool ov)
-{
-    if (ov) return qclass == 0 ? k_score_tiles<1, 16, true> : qclass == 1 ? k_score_tiles<1, 24, true> : k_score_tiles<1, 32, true>;
-    if (flavor == 0) return qclass == 0 ? k_score_tiles<0, 16, false> : qclass == 1 ? k_score_tiles<0, 24, false> : k_score_tiles<0, 32, false>;
-    if (flavor == 2) return qclass == 0 ? k_score_tiles<2, 16, false> : qclass == 1 ? k_score_tiles<2, 24, false> : k_score_tiles<2, 32, false>;
-    if (flavor == 3) return qclass == 0 ? k_score_tiles<3, 16, false> : qclass == 1 ? k_score_tiles<3, 24, false> : k_score_tiles<3, 32, false>;
-    return qclass == 0 ? k_score_tiles<1, 16, false> : qclass == 1 ? k_score_tiles<1, 24, false> : k_score_tiles<1, 32, false>;
-}
-// mode 0: uniform scheme, 1: sparse overrides, 2: dense table
-size_t tile_smem(int mode) { return mode == 1 ? sizeof(nwap_tile_smem_t<1>) : mode == 2 ? sizeof(nwap_tile_smem_t<2>) : sizeof(nwap_tile_smem_t<0>); }
-
 // Device facts, kernel attributes and the memory-pool policy: once per device per process.
 int ensure_device_cache(int device, device_cache **out)
 {
@@ -142,10 +179,10 @@ int ensure_device_cache(int device, device_cache **out)
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
         unsigned long long keep = ~0ull;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-        for (int f = 0; f < 5; ++f)          // f == 3: sparse-override build, f == 4: dense-table build
+        for (int f = 0; f < NWAP_TILE_FAMILIES; ++f)
             for (int w = 0; w < 3; ++w) {
-                tile_kernel_t k = tile_kernel(f == 3 ? 1 : f == 4 ? 3 : f, w, f == 3);
-                const size_t smem = tile_smem(f == 3 ? 1 : f == 4 ? 2 : 0);
+                nwap_tile_kernel_t k = nwap_tile_kernel(f, w);
+                const size_t smem = nwap_tile_smem_bytes(f);
                 CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 int occ = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem));
@@ -224,28 +261,37 @@ int fetch_stats(nwap_ctx *c, nwap_stats *out, cudaStream_t st)
 }
 
 // Enqueue the scoring of [start, end) into out_dev on `st`.  Statistics accumulate
-// into c->d_stats (caller resets).  No synchronisation.
+// into c->d_stats (caller resets).  No synchronisation.  `sparse` (may be NULL) switches the
+// tile kernel's writer to sparse output; out_dev may then be NULL (no dense payload).
 int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int want_hist,
-                  int variant, cudaStream_t st)
+                  int variant, cudaStream_t st, const nwap_sparse_out *sparse = nullptr)
 {
     if (start >= end) return NWAP_OK;
-    const bool fast_ok = (!c->general || c->sparse_ov) && c->qmax <= NWAP_MAXLEN_FAST;
+    const bool uniform_ok = !c->general || c->sparse_ov;
+    const bool fast_ok = uniform_ok && c->qmax <= NWAP_MAXLEN_FAST;
+    const bool wide_ok = !c->general && c->qmax <= NWAP_MAXLEN_WIDE;          // block-wise path: uniform schemes only
     const bool tab_ok = c->general && c->tab_ok && c->qmax <= NWAP_MAXLEN_FAST;
     const bool sym_ok = fast_ok && !c->general && nwap_flavor2_ok(c->match, c->mismatch);
     // PACKED3 (2 DPX + IMAD + IADD) is ~8 % faster than PACKED (2 DPX + 2 IMAD) and ~14 % faster than PACKED_SYM
     // (2 DPX + IADD3: one issue fewer, but IADD3 shares the DPX pipe): profiles/r01f_ab_packed_sym.txt
-    // override tables: the table-driven cell (4.8 TCUPS) beats the sparse-correction cell (2.7 TCUPS with six overridden
-    // pairs, profiles/r01_ov_bench.txt) whenever the alphabet fits shared memory, so `auto` takes it first
+    // override tables: the table-driven cell beats the sparse-correction cell whenever the alphabet fits shared
+    // memory, so `auto` takes it first.  A uniform scheme never leaves the packed kernel: the preflight admits at
+    // most 64 symbols per word (gap -1, engine.py:83-90), which the wide build covers.
     if (variant == NWAP_VARIANT_AUTO)
-        variant = tab_ok ? NWAP_VARIANT_PACKED_TAB : fast_ok ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
+        variant = tab_ok ? NWAP_VARIANT_PACKED_TAB : (fast_ok || wide_ok) ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
     if (variant == NWAP_VARIANT_PACKED_TAB && !tab_ok)
         return fail(NWAP_EINVAL, "packed_tab kernel needs a dense similarity table with K <= %d and max word length <= %d", NWAP_OV_MAXK, NWAP_MAXLEN_FAST);
     if (variant == NWAP_VARIANT_PACKED_SYM && !sym_ok)
         return fail(NWAP_EINVAL, "packed_sym kernel needs a uniform scheme with match >= mismatch and max word length <= %d (have %d%s)",
                     NWAP_MAXLEN_FAST, c->qmax, c->general ? ", similarity overrides" : "");
-    if ((variant == NWAP_VARIANT_PACKED || variant == NWAP_VARIANT_PACKED3) && !fast_ok)
+    if (variant == NWAP_VARIANT_PACKED && !fast_ok)
         return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme (or at most %d overrides per symbol) and max word length <= %d (have %d%s)",
                     NWAP_MAX_OV, NWAP_MAXLEN_FAST, c->qmax, c->general ? ", dense similarity table" : "");
+    if (variant == NWAP_VARIANT_PACKED3 && !fast_ok && !wide_ok)
+        return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme and max word length <= %d, or at most %d overrides per symbol and max word length <= %d (have %d%s)",
+                    NWAP_MAXLEN_WIDE, NWAP_MAX_OV, NWAP_MAXLEN_FAST, c->qmax, c->general ? ", similarity table" : "");
+    if (sparse && (variant != NWAP_VARIANT_PACKED3 || c->general))
+        return fail(NWAP_EINVAL, "sparse output is built for the default packed kernel and uniform schemes");
 
     if (variant == NWAP_VARIANT_SIMPLE) {
         nwap_simple_params p;
@@ -266,7 +312,9 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     const bool tab = variant == NWAP_VARIANT_PACKED_TAB;
     const bool ov = c->general && !tab;               // here: general and not tab implies sparse_ov
     const int flavor = tab ? 3 : variant == NWAP_VARIANT_PACKED_SYM ? 2 : (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
-    const int qclass = c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
+    const bool wide = flavor == 1 && !ov && c->qmax > NWAP_WIDE_FROM;
+    const int qclass = wide ? 1 : c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
+    const int family = wide ? (sparse ? 7 : 5) : sparse ? 6 : ov ? 3 : tab ? 4 : flavor;
     nwap_tile_params p;
     p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad;
     p.start = start; p.end = end;
@@ -281,8 +329,10 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.unit_counter = c->d_counter;
     p.ov_table = ov ? c->d_ov : nullptr; p.ov_K = (ov || tab) ? c->K : 0;
     p.etab = tab ? c->d_etab : nullptr;
+    if (sparse) p.sparse = *sparse;
+    else memset(&p.sparse, 0, sizeof p.sparse);
 
-    const int occ = std::max(1, c->occ_tiles[(ov ? 3 : tab ? 4 : flavor) * 3 + qclass]);
+    const int occ = std::max(1, c->occ_tiles[family * 3 + qclass]);
     const int64_t slots = (int64_t)c->sm_count * occ;
     // bands per group: as large as possible (amortises the per-unit sort) while
     // leaving >= 24 units per resident CTA for dynamic balance.
@@ -301,7 +351,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.us = us; p.unit_begin = ubeg; p.unit_count = ucount;
     const int64_t grid = std::min<int64_t>(slots, ucount);
     CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
-    tile_kernel(flavor, qclass, ov)<<<(unsigned)grid, NWAP_THREADS, tile_smem(ov ? 1 : tab ? 2 : 0), st>>>(p);
+    nwap_tile_kernel(family, qclass)<<<(unsigned)grid, NWAP_THREADS, nwap_tile_smem_bytes(family), st>>>(p);
     g_launches++;
     CK(cudaGetLastError());
     return NWAP_OK;
@@ -354,7 +404,7 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
         if (len < 1) return fail(NWAP_EINVAL, "word %lld is empty (length 0)", (long long)i);
         for (int j = 0; j < len; ++j) maxsym = std::max<int>(maxsym, ids[i * q_stride + j]);
     }
-    CK(cudaSetDevice(device));
+    ON_DEVICE(device);
     device_cache *dc = nullptr;
     {
         const int rc0 = ensure_device_cache(device, &dc);
@@ -415,7 +465,7 @@ int nwap_set_similarity(nwap_ctx *c, const int8_t *sim, int K)
         }
     int q = nwap_preflight(c->h_lens.data(), c->n, c->gap, mn, mx, nullptr, nullptr);
     if (q < 0) return q;
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     c->K = K;
     c->general = true;
     // uniform + sparse corrections?  then the packed kernel can run it
@@ -445,10 +495,12 @@ int nwap_set_similarity(nwap_ctx *c, const int8_t *sim, int K)
 void nwap_destroy(nwap_ctx *c)
 {
     if (!c) return;
-    cudaSetDevice(c->device);
+    device_guard guard_(c->device);
     cudaDeviceSynchronize();             // nothing may still be reading the store or writing the slabs
     dev_free(c->d_ids); dev_free(c->d_lens); dev_free(c->d_sim); dev_free(c->d_stats); dev_free(c->d_ov); dev_free(c->d_etab);
     dev_free(c->d_counter); dev_free(c->d_block_counts); dev_free(c->d_total);
+    dev_free(c->d_kept); dev_free(c->d_kbounds);
+    cudaFree(c->d_keys); cudaFree(c->d_sort_table);
     if (c->pipe) {                       // back to the device cache for the next context
         std::lock_guard<std::mutex> lock(g_cache_mutex);
         g_cache[c->device].free_pipes.push_back(c->pipe);
@@ -506,7 +558,7 @@ int nwap_score_range(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, n
     const int64_t P = nwap_num_edges(c);
     if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
     if (start < end && !out_dev) return fail(NWAP_EINVAL, "null output buffer");
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     cudaStream_t st = (cudaStream_t)stream;
     int rc = reset_stats(c, st);
     if (rc) return rc;
@@ -519,7 +571,7 @@ int nwap_score_range(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, n
 int nwap_read_stats(nwap_ctx *c, nwap_stats *stats_host, void *stream)
 {
     if (!c || !stats_host) return fail(NWAP_EINVAL, "null argument");
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     return fetch_stats(c, stats_host, (cudaStream_t)stream);
 }
 
@@ -530,7 +582,7 @@ int nwap_score_range_host_begin(nwap_ctx *c, int64_t start, int64_t end, int8_t 
     const int64_t P = nwap_num_edges(c);
     if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
     if (start < end && !out_host) return fail(NWAP_EINVAL, "null output buffer");
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     const int64_t total = end - start;
     // slab: large enough to amortise launches, small enough that the first copy starts early
     int64_t slab = std::max<int64_t>(int64_t(8) << 20, std::min<int64_t>(int64_t(256) << 20, (total + 7) / 8));
@@ -566,7 +618,7 @@ int nwap_score_range_host_wait(nwap_ctx *c, nwap_stats *stats_host)
     if (!c) return fail(NWAP_EINVAL, "null context");
     if (!c->host_pending) return fail(NWAP_EINVAL, "no host-destination call in flight on this context");
     c->host_pending = false;
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     nwap_pipe *p = c->pipe;
     CK(cudaStreamSynchronize(p->s_copy));
     if (stats_host) return fetch_stats(c, stats_host, p->s_compute);
@@ -586,7 +638,7 @@ int nwap_payload_stats(nwap_ctx *c, const int8_t *payload_dev, int64_t count, nw
 {
     if (!c || !stats_host) return fail(NWAP_EINVAL, "null argument");
     if (count < 0 || (count > 0 && !payload_dev)) return fail(NWAP_EINVAL, "bad payload");
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     cudaStream_t st = (cudaStream_t)stream;
     int rc = reset_stats(c, st);
     if (rc) return rc;
@@ -611,7 +663,7 @@ static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start,
     const int64_t count = end - start;
     if (count == 0) return NWAP_OK;
     if (!payload_dev) return fail(NWAP_EINVAL, "null payload");
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     // blocks tile the 16-byte aligned window that contains the slice (k_compact_*: nwap_cmp_first)
     const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload_dev) & 15u);
     const int64_t nblocks = (lead + count + NWAP_CMP_BLOCK - 1) / NWAP_CMP_BLOCK;
@@ -653,6 +705,108 @@ int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, in
                           (cudaStream_t)stream);
 }
 
+// Sparse-output scoring (the edge writer with threshold compaction fused in): score [start, end), keep what the
+// predicate keeps, restore index order, unpack.  mode 1: raw threshold, mode 2: normalised-weight bounds.
+static int score_sparse_common(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int mode, int threshold,
+                               double lo, double hi, int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap,
+                               int64_t *count_host, int32_t *degree_dev, nwap_stats *stats_host, int variant,
+                               cudaStream_t st)
+{
+    if (!c || !count_host) return fail(NWAP_EINVAL, "null argument");
+    const int64_t P = nwap_num_edges(c);
+    if (start < 0 || end > P || start > end) return fail(NWAP_EINVAL, "range [%lld, %lld) outside [0, %lld)", (long long)start, (long long)end, (long long)P);
+    if (cap < 0 || cap > 0x7fffffffLL || (cap > 0 && (!idx_out_dev || !score_out_dev))) return fail(NWAP_EINVAL, "bad output buffers (capacity must be in [0, 2^31))");
+    if (P >= (int64_t(1) << 55)) return fail(NWAP_EINVAL, "too many edges for the 56-bit index keys of the sparse output");
+    *count_host = 0;
+    ON_DEVICE(c->device);
+    if (!c->d_kept) {
+        CK(dev_alloc(&c->d_kept, sizeof(unsigned long long)));
+        CK(dev_alloc(&c->d_kbounds, sizeof(short2) * 256));
+    }
+    if (c->keys_cap < cap) {
+        CK(cudaDeviceSynchronize());
+        cudaFree(c->d_keys); c->d_keys = nullptr; c->keys_cap = 0;
+        if (cudaMalloc(&c->d_keys, sizeof(unsigned long long) * (size_t)cap) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(NWAP_ENOMEM, "cudaMalloc of the %lld-entry key scratch failed", (long long)cap);
+        }
+        c->keys_cap = cap;
+    }
+    nwap_sparse_out so;
+    memset(&so, 0, sizeof so);
+    so.mode = mode; so.threshold = threshold; so.keys = reinterpret_cast<unsigned long long *>(idx_out_dev);
+    so.cap = cap; so.count = c->d_kept; so.degree = degree_dev; so.bounds = c->d_kbounds;
+    if (mode == 2) {
+        nwap_keep_params kp;
+        nwap_fill_norm_bounds(kp, lo, hi);
+        short2 hb[256];
+        for (int m = 0; m < 256; ++m) hb[m] = make_short2(kp.smin[m], kp.smax[m]);
+        so.gmin = kp.gmin; so.gmax = kp.gmax;
+        CK(cudaMemcpyAsync(c->d_kbounds, hb, sizeof hb, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));          // hb is a stack temporary
+    }
+    int rc = reset_stats(c, st);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(c->d_kept, 0, sizeof(unsigned long long), st));
+    rc = enqueue_score(c, start, end, out_dev, 0, variant, st, &so);
+    if (rc) return rc;
+    unsigned long long kept = 0;
+    CK(cudaMemcpyAsync(&kept, c->d_kept, sizeof kept, cudaMemcpyDeviceToHost, st));
+    if (stats_host) { rc = fetch_stats(c, stats_host, st); if (rc) return rc; }
+    else CK(cudaStreamSynchronize(st));
+    *count_host = (int64_t)kept;
+    if ((int64_t)kept > cap) return fail(NWAP_ECAPACITY, "sparse output kept %lld edges but capacity is %lld", (long long)kept, (long long)cap);
+    if (kept == 0) return NWAP_OK;
+    // restore index order: LSD radix sort of the index bits (the low 8 bits of a key are the score)
+    const long long n = (long long)kept;
+    long long tile = NWAP_SORT_TILE;
+    if ((n + tile - 1) / tile > 65536) tile = (((n + 65535) / 65536) + 31) / 32 * 32;
+    const long long ntiles = (n + tile - 1) / tile;
+    if (c->sort_table_cap < 256 * ntiles) {
+        CK(cudaDeviceSynchronize());
+        cudaFree(c->d_sort_table); c->d_sort_table = nullptr; c->sort_table_cap = 0;
+        if (cudaMalloc(&c->d_sort_table, sizeof(unsigned int) * (size_t)(256 * ntiles)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(NWAP_ENOMEM, "cudaMalloc of the sort table failed");
+        }
+        c->sort_table_cap = 256 * ntiles;
+    }
+    int bits = 1;
+    while (bits < 55 && (int64_t(1) << bits) < P) ++bits;
+    unsigned long long *src = so.keys, *dst = c->d_keys;
+    const unsigned sblocks = (unsigned)((ntiles + NWAP_SORT_WARPS - 1) / NWAP_SORT_WARPS);
+    for (int shift = 8; shift < 8 + bits; shift += 8) {
+        k_sort_hist<<<sblocks, NWAP_SORT_WARPS * 32, 0, st>>>(src, n, shift, c->d_sort_table, ntiles, tile);
+        k_sort_scan<<<1, 1024, 0, st>>>(c->d_sort_table, 256 * ntiles);
+        k_sort_scatter<<<sblocks, NWAP_SORT_WARPS * 32, 0, st>>>(src, dst, n, shift, c->d_sort_table, ntiles, tile);
+        g_launches += 3;
+        std::swap(src, dst);
+    }
+    const unsigned ublocks = (unsigned)std::min<long long>((n + 255) / 256, (long long)c->sm_count * 8);
+    k_sort_unpack<<<ublocks, 256, 0, st>>>(src, n, (long long *)idx_out_dev, (signed char *)score_out_dev);
+    g_launches++;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return NWAP_OK;
+}
+
+int nwap_score_range_compact(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int threshold,
+                             int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
+                             int32_t *degree_dev, nwap_stats *stats_host, int variant, void *stream)
+{
+    return score_sparse_common(c, start, end, out_dev, 1, threshold, 0.0, 0.0, idx_out_dev, score_out_dev, cap, count_host,
+                               degree_dev, stats_host, variant, (cudaStream_t)stream);
+}
+
+int nwap_score_range_filter_normalized(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, double lo, double hi,
+                                       int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
+                                       int32_t *degree_dev, nwap_stats *stats_host, int variant, void *stream)
+{
+    if (lo > hi) return fail(NWAP_EINVAL, "empty filter range: lo=%g > hi=%g", lo, hi);
+    return score_sparse_common(c, start, end, out_dev, 2, 0, lo, hi, idx_out_dev, score_out_dev, cap, count_host,
+                               degree_dev, stats_host, variant, (cudaStream_t)stream);
+}
+
 int nwap_filter_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end, double lo, double hi,
                            int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
                            int32_t *degree_dev, void *stream)
@@ -675,7 +829,7 @@ int nwap_hist_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, 
     const int64_t count = end - start;
     if (count == 0) return NWAP_OK;
     if (!payload_dev) return fail(NWAP_EINVAL, "null payload");
-    CK(cudaSetDevice(c->device));
+    ON_DEVICE(c->device);
     cudaStream_t st = (cudaStream_t)stream;
     nwap_keep_params kp;
     kp.threshold = 0; memset(kp.smin, 0, sizeof kp.smin); memset(kp.smax, 0, sizeof kp.smax); kp.gmin = 0; kp.gmax = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
@@ -733,7 +887,7 @@ int nwap_rows_cols(int64_t n, const int64_t *idx_dev, int64_t count, int64_t *ro
 int nwap_probe(int device, int which, int iters, double *ipc_out, double *ms_out)
 {
     if (which < 0 || which >= NWAP_PROBE_COUNT || iters < 1 || !ipc_out || !ms_out) return fail(NWAP_EINVAL, "bad argument");
-    CK(cudaSetDevice(device));
+    ON_DEVICE(device);
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     const int blocks = prop.multiProcessorCount;

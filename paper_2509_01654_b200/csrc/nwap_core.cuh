@@ -434,6 +434,63 @@ NWAP_HD void nwap_dp_word_tab(const nwap_sym2 *row_sym2, int la, const uint32_t 
     } while (s != e);
 }
 
+// ---- column words longer than the register-resident row (24 < length <= 64) -------------------
+// The int8 preflight admits words of up to 64 symbols for gap -1 -- the paper's own scheme
+// (1,-1,-1), reference engine.py:83-90 -- but a 64-column rolling row plus 64 packed symbols
+// does not fit the register budget of two 320-thread CTAs per SM.  Such chunks are scored in
+// blocks of NWAP_WB columns: block k is the same software-pipelined row update at register
+// width NWAP_WB whose left boundary is not the matrix border but column NWAP_WB*k of the same
+// matrix row, saved by block k-1 (one 32-bit word per matrix row per lane, `save`).  The
+// recurrence H'[i][j] = max(H'[i-1][j-1] - e*D, H'[i-1][j] + u, H'[i][j-1]) holds at every j,
+// so (d0, left0) = (H'[i-1][WB*k], H'[i][WB*k]) is all a block needs from its left neighbour.
+// b0 / b1: the two column words' symbols, readable (padding included) up to NWAP_WB*nblk bytes.
+// Returns the packed H'[la][l0] | H'[la][l1] << 16.
+#define NWAP_WB 16
+#define NWAP_MAXLEN_WIDE 64
+
+NWAP_HD void nwap_load_block_negb(const uint8_t *b0, const uint8_t *b1, uint32_t (&nb)[NWAP_WB])
+{
+#if defined(__CUDA_ARCH__)
+    const uint4 x = __ldg(reinterpret_cast<const uint4 *>(b0));
+    const uint4 y = __ldg(reinterpret_cast<const uint4 *>(b1));
+    const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, yw[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int j = 0; j < NWAP_WB; ++j)
+        nb[j] = nwap_pack_negb((xw[j >> 2] >> (8 * (j & 3))) & 0xffu, (yw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+#else
+    for (int j = 0; j < NWAP_WB; ++j) nb[j] = nwap_pack_negb(b0[j], b1[j]);
+#endif
+}
+
+NWAP_HD uint32_t nwap_dp_blocks(const nwap_sym2 *row_sym2, int la, const uint8_t *b0, const uint8_t *b1, int nblk,
+                                int l0, int l1, const nwap_scheme_consts &sc, uint32_t *save)
+{
+    uint32_t lo = 0, hi = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+        uint32_t nb[NWAP_WB];
+        nwap_load_block_negb(b0 + NWAP_WB * blk, b1 + NWAP_WB * blk, nb);
+        uint32_t P[NWAP_WB + 1];
+#pragma unroll
+        for (int j = 0; j <= NWAP_WB; ++j) P[j] = NWAP_BIAS2;      // H'[0][j]
+        uint32_t d0 = NWAP_BIAS2;                                  // H'[0][WB*blk]
+#pragma unroll 1
+        for (int i = 0; i < la; ++i) {
+            const nwap_sym2 x = row_sym2[i];
+            const uint32_t left0 = blk == 0 ? x.left0 : save[i];   // H'[i+1][WB*blk]
+            nwap_dp_row<NWAP_WB, 1>(x.a2, nb, P, d0, left0, sc);
+            d0 = left0;
+            save[i] = P[NWAP_WB];                                  // H'[i+1][WB*(blk+1)] for the next block
+        }
+        const int j0 = l0 - NWAP_WB * blk, j1 = l1 - NWAP_WB * blk;
+#pragma unroll
+        for (int j = 1; j <= NWAP_WB; ++j) {
+            if (j == j0) lo = P[j] & 0xffffu;
+            if (j == j1) hi = P[j] & 0xffff0000u;
+        }
+    }
+    return lo | hi;
+}
+
 // Whole pair-of-pairs DP for one row word; returns the packed H' values at
 // (la, lb0) in the low half and (la, lb1) in the high half.  Used by the host
 // emulation test; the tile kernel calls nwap_dp_word directly.

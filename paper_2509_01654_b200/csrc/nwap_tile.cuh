@@ -1,0 +1,881 @@
+// nwap_tile.cuh -- the hot kernel of the all-pairs NW scoring path (k_score_tiles) and what it shares with the
+// consumers.  Templates and inline device code only: included by every tiles_*.cu instantiation unit.
+// (kernel inventory of the whole library:)
+//
+//   k_score_tiles<FLAVOR,QMAX>  the hot kernel: persistent 10-warp CTAs (two per SM) over (strip, band-group)
+//                               work units; per unit the strip's 5120 columns are counting-sorted by word
+//                               length in shared memory, warps pull 64-column chunks longest-first (so the
+//                               warps of a CTA sit in neighbouring length-specialised bodies), each lane
+//                               scores 2 pairs per register (s16x2 DPX); one length dispatch per chunk, the
+//                               body owning the loop over the band's 16 rows; results are staged in shared
+//                               memory at their ORIGINAL column and flushed as coalesced 16-byte stores.
+//                               Replaces reference engine.py:176-195 (_score_range) with
+//                               triangle.py:93-112 folded in (one index recovery per row).
+//   k_score_simple              one thread per pair, int32 cells, K x K similarity table:
+//                               any scheme (overrides), any q <= 255.  Generic path and the
+//                               independent second implementation used for cross-checks.
+//   k_payload_stats             sum/min/max/count/hist of a dense payload (store.py:342-381 raw).
+//   k_compact_*                 ordered threshold compaction + degree counts (graph.py:97-101).
+//   k_rows_cols                 triangle.py:93-112 exposed for parity tests.
+//   k_probe<W>                  instruction-issue probes for the integer roofline.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "nwap_core.cuh"
+#include "nwap_index.cuh"
+
+#ifndef NWAP_LBSTEP
+#define NWAP_LBSTEP 1
+#endif
+#ifndef NWAP_MINB
+#define NWAP_MINB 2               // resident CTAs/SM the register allocator must allow
+#endif
+#ifndef NWAP_UNITS_PER_SLOT
+#define NWAP_UNITS_PER_SLOT 48
+#endif
+#define NWAP_WARPS (NWAP_THREADS / 32)
+#define NWAP_PITCH (NWAP_C + 16)         // bytes per staged output row (multiple of 16)
+#define NWAP_MAXLEN_FAST 32              // register-resident row limit
+#ifndef NWAP_WIDE_FROM
+#define NWAP_WIDE_FROM 32                // vocabularies whose longest word exceeds this run the wide build
+#endif
+
+struct nwap_dev_stats {                   // same layout as nwap_stats
+    long long sum;
+    long long count;
+    int mn;
+    int mx;
+    unsigned long long hist[256];
+};
+
+// ---------------------------------------------------------------------------
+// Keep predicate of the threshold compaction / normalised-weight filter (graph.py:91-101), shared by the
+// dense-payload consumers (k_compact_*) and the tile kernel's sparse-output mode.
+// ---------------------------------------------------------------------------
+struct nwap_keep_params {
+    int threshold;           // MODE 0
+    const uint8_t *lens;     // MODE 1
+    int64_t n;
+    int64_t start;           // linear index of payload[0]
+    // MODE 1: for every m = max(len_r, len_c) the scores s with lo <= 100.0*s/m <= hi form an interval
+    // [smin[m], smax[m]] (the quotient is monotonic in s).  The host fills the table by evaluating the
+    // reference's IEEE-double expression (graph.py:96-98) for all 256 x 255 (s, m), so the device test is
+    // two integer compares and exactly the reference's keep-mask; an empty interval is smin > smax.
+    int8_t smin[256], smax[256];
+    int gmin, gmax;          // MODE 1: loosest bounds over all lengths (gmin > gmax: nothing can be kept)
+};
+
+// host side of the table above
+inline void nwap_fill_norm_bounds(nwap_keep_params &kp, double lo, double hi)
+{
+    for (int m = 0; m < 256; ++m) {
+        int first = 1, last = 0;                     // empty
+        bool any = false;
+        for (int sc = -128; sc <= 127 && m > 0; ++sc) {
+            const double w = (100.0 * (double)sc) / (double)m;
+            if (w >= lo && w <= hi) { if (!any) first = sc; last = sc; any = true; }
+        }
+        kp.smin[m] = (int8_t)first;
+        kp.smax[m] = (int8_t)last;
+    }
+    kp.gmin = 127; kp.gmax = -128;
+    for (int m = 1; m < 256; ++m)
+        if (kp.smin[m] <= kp.smax[m]) { kp.gmin = kp.gmin < kp.smin[m] ? kp.gmin : kp.smin[m]; kp.gmax = kp.gmax > kp.smax[m] ? kp.gmax : kp.smax[m]; }
+}
+
+// MODE 0: bit j of the result = (signed byte j of the 4 words >= threshold), 4 bytes per SWAR step.
+// x = w ^ 0x80808080 orders the bytes as unsigned; T = threshold + 128 in [0, 255].
+__device__ __forceinline__ unsigned nwap_ge_bits4(uint32_t w, uint32_t tl_rep, bool th)
+{
+    const uint32_t x = w ^ 0x80808080u;
+    const uint32_t d = ((x & 0x7f7f7f7fu) | 0x80808080u) - tl_rep;     // bit 7 of a byte: low 7 bits >= low 7 bits of T
+    const uint32_t m = (th ? (x & d) : (x | d)) & 0x80808080u;
+    return (((m >> 7) * 0x01020408u) >> 24) & 0xfu;
+}
+
+// Sparse-output mode of the tile kernel (BASELINE north_star: "the int8 edge writer, with optional
+// score-threshold compaction"): kept edges leave the kernel as unordered 64-bit keys
+// (linear index << 8 | score byte) appended through one global counter; a radix sort of the keys
+// restores index order afterwards (k_sort_*).  The dense payload need not exist at all.
+struct nwap_sparse_out {
+    int mode;                       // 0: off, 1: raw score >= threshold, 2: normalised-weight bounds (graph.py:96-98)
+    int threshold;                  // mode 1
+    int gmin, gmax;                 // mode 2: loosest score bounds over all lengths (candidates)
+    const short2 *bounds;           // mode 2: device table of 256 per-length (smin, smax)
+    unsigned long long *keys;       // device, `cap` entries
+    long long cap;
+    unsigned long long *count;      // device counter (may exceed cap: the excess is dropped, the host reports it)
+    int *degree;                    // device (n,) or NULL: +1 at both endpoints of every kept edge
+};
+
+struct nwap_tile_params {
+    const uint8_t *ids;      // (n, qpad) uint8
+    const uint8_t *lens;     // (n padded to strips) uint8, zero beyond n
+    int64_t n;
+    int qpad;
+    int64_t start, end;      // linear range
+    int64_t r_first, r_last; // rows holding start and end-1
+    int64_t c_start, c_end;  // column of start, column of end-1 (inclusive)
+    int8_t *out;             // out[k - start]
+    nwap_scheme_consts sc;
+    nwap_unit_space us;
+    int64_t unit_begin;      // absolute id of the first unit of this launch
+    int64_t unit_count;
+    unsigned long long *unit_counter;
+    nwap_dev_stats *stats;
+    int want_hist;
+    const nwap_ov_row *ov_table;   // sparse-override mode: (ov_K) rows on the device, else NULL
+    int ov_K;                      // alphabet size K of the override / dense table
+    const uint8_t *etab;           // dense-table mode (FLAVOR 3): K x K table of M - sim on the device, else NULL
+    nwap_sparse_out sparse;        // CMP instantiations only
+};
+
+struct alignas(16) nwap_row_meta {
+    // first 16 bytes: everything the fast row path needs, one LDS.128
+    int la;            // row word length, 0 = row not in this launch / no valid column in this strip
+    uint32_t ala2;     // (alpha * la) * 65537: the row potential, packed for both halves
+    int rowadj;        // smem byte index of (column offset 0): rr*PITCH + skew - clo_off
+    int skew;          // (global address of the segment) & 15
+    int clo_off;       // first valid column, relative to the strip
+    int seglen;        // number of valid columns in this strip for this row
+    int64_t g0;        // out-relative byte offset of the segment
+};
+
+// ---------------------------------------------------------------------------
+// shared memory carve-up of k_score_tiles
+// ---------------------------------------------------------------------------
+#define NWAP_OV_MAXK 128               // largest alphabet the sparse-override table holds in shared memory
+template <int MODE> struct nwap_sym_of { typedef nwap_sym2 type; };
+template <> struct nwap_sym_of<1> { typedef nwap_sym4 type; };
+
+// MODE 0: uniform scheme, 1: sparse overrides (per-symbol correction rows), 2: dense table (K x K bytes of M - sim)
+// MAXLEN: longest word the instantiation accepts (32, or 64 for the block-wise wide build)
+template <int MODE, int MAXLEN = NWAP_MAXLEN_FAST>
+struct nwap_tile_smem_t {
+    alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
+    typedef typename nwap_sym_of<MODE>::type sym_t;
+    alignas(16) sym_t rowsym[NWAP_R][MAXLEN + 1];                // {a*65537, H'[i+1][0] (, override row)} per matrix row
+    alignas(16) nwap_ov_row ov[MODE == 1 ? NWAP_OV_MAXK : 1];       // per-symbol override table (sparse-override mode)
+    alignas(16) uint8_t etab[MODE == 2 ? NWAP_OV_MAXK * NWAP_OV_MAXK : 16];   // dense-table mode
+    alignas(16) nwap_row_meta meta[NWAP_R];
+    uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
+    uint8_t clen[NWAP_C];         // their lengths
+    int bins[NWAP_WARPS][MAXLEN + 2];
+    unsigned int hist[256];
+    short2 kbounds[256];          // sparse-output mode, normalised filter: per-length score bounds
+    unsigned long long unit;
+    long long sum;
+    long long count;
+    int mn, mx;
+    int ncols;
+    int next_chunk;
+};
+
+typedef nwap_tile_smem_t<0> nwap_tile_smem;
+
+__device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
+{
+    return (w[j >> 2] >> (8 * (j & 3))) & 0xffu;
+}
+
+// Statistics are kept packed: t = H' + row potential + column potential has halves
+// score + BIAS, so min/max are one VIMNMX.S16x2 each for both pairs and the byte to store
+// is simply the low byte of each half (BIAS is a multiple of 256).
+struct nwap_lane_stats {
+    uint32_t mn2, mx2;      // packed running min / max of (score + BIAS)
+    long long sum;          // sum of scores
+    int count;              // valid pairs
+};
+
+// One lane's two columns of a 64-column chunk.
+struct nwap_lane_cols {
+    uint32_t off0, off1;    // strip-relative column offsets (0xffff = no column)
+    int l0, l1;             // word lengths
+    uint32_t kpos2;         // column potentials, packed (BIAS stays in: halves of t are score + BIAS)
+    uint32_t keep_v;        // per-half mask: 0xffff where the word has length LB
+    uint32_t keep_1;        // per-half mask: 0xffff where the word has length LB-1 (else LB-2 in mixmode 2)
+};
+
+__device__ __forceinline__ nwap_lane_cols nwap_make_lane_cols(uint32_t off0, uint32_t off1, int l0, int l1, int LB,
+                                                              const nwap_scheme_consts &sc)
+{
+    nwap_lane_cols c;
+    c.off0 = off0; c.off1 = off1; c.l0 = l0; c.l1 = l1;
+    c.kpos2 = (uint32_t)(sc.beta * l0) + ((uint32_t)(sc.beta * l1) << 16);
+    c.keep_v = (l0 == LB ? 0xffffu : 0u) | (l1 == LB ? 0xffff0000u : 0u);
+    c.keep_1 = (l0 == LB - 1 ? 0xffffu : 0u) | (l1 == LB - 1 ? 0xffff0000u : 0u);
+    return c;
+}
+
+// Per-chunk packed accumulators of t (<= 2 * 16 rows: no overflow of either half-sum).
+struct nwap_chunk_acc { uint32_t acc, acc_hi; int rows_fast; };
+
+// Score fix-up, staging store and statistics of one packed result (shared by all lengths).
+template <class SM>
+__device__ __forceinline__ void nwap_emit(SM &sm, const nwap_row_meta &m, uint32_t ala2, int adj, uint32_t v,
+                                          const nwap_lane_cols &c, bool fast, int want_hist,
+                                          nwap_lane_stats &ls, nwap_chunk_acc &ca)
+{
+    const uint32_t t = v + ala2 + c.kpos2;          // halves: score + BIAS (never negative)
+    const uint32_t thi = t >> 16;
+    if (fast) {
+        sm.out[adj + (int)c.off0] = (uint8_t)t;
+        sm.out[adj + (int)c.off1] = (uint8_t)thi;
+        ls.mn2 = __vmins2(ls.mn2, t);
+        ls.mx2 = __vmaxs2(ls.mx2, t);
+        ca.acc += t;
+        ca.acc_hi += thi;
+        ++ca.rows_fast;
+    } else {
+        const uint32_t clo = (uint32_t)m.clo_off;
+        const uint32_t seg = (uint32_t)m.seglen;
+        const int s0 = (int)(t & 0xffffu) - (int)NWAP_BIAS;
+        const int s1 = (int)thi - (int)NWAP_BIAS;
+        if (c.off0 - clo < seg) {
+            sm.out[adj + (int)c.off0] = (uint8_t)(int8_t)s0;
+            ls.sum += s0; ls.count += 1;
+            ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffff0000u) | (t & 0xffffu));
+            ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffff0000u) | (t & 0xffffu));
+            if (want_hist) atomicAdd(&sm.hist[(s0 + 128) & 255], 1u);
+        }
+        if (c.off1 - clo < seg) {
+            sm.out[adj + (int)c.off1] = (uint8_t)(int8_t)s1;
+            ls.sum += s1; ls.count += 1;
+            ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffffu) | (t & 0xffff0000u));
+            ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffffu) | (t & 0xffff0000u));
+            if (want_hist) atomicAdd(&sm.hist[(s1 + 128) & 255], 1u);
+        }
+    }
+}
+
+__device__ __forceinline__ void nwap_close_chunk(nwap_lane_stats &ls, const nwap_chunk_acc &ca)
+{
+    if (ca.rows_fast) {
+        // acc = sum(lo) + 65536 * sum(hi) (mod 2^32), acc_hi = sum(hi): both sums < 2^19
+        const uint32_t sum_lo = ca.acc - (ca.acc_hi << 16);
+        ls.sum += (long long)sum_lo + (long long)ca.acc_hi - 2ll * ca.rows_fast * (long long)NWAP_BIAS;
+        ls.count += 2 * ca.rows_fast;
+    }
+}
+
+// mixmode 1/2: pick the final cell of each half among the last three columns (bitwise selects)
+__device__ __forceinline__ uint32_t nwap_merge3(uint32_t v, uint32_t vm1, uint32_t vm2, const nwap_lane_cols &c)
+{
+    const uint32_t t = (vm1 & c.keep_1) | (vm2 & ~c.keep_1);
+    return (v & c.keep_v) | (t & ~c.keep_v);
+}
+
+struct nwap_true { __device__ constexpr operator bool() const { return true; } };
+struct nwap_false { __device__ constexpr operator bool() const { return false; } };
+
+// The only length-specialised code: the DP of one row word at register width LB.  Returns the
+// final cells for words of length LB (v) and LB-1 (vm1) -- all a sorted chunk normally
+// contains; `deep` (a chunk spanning three or more lengths: the long and short tails of a
+// strip) selects per lane among all columns.
+template <int LB, int FLAVOR>
+__device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym2 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                                                 const nwap_scheme_consts &sc, const nwap_ov_row *)
+{
+    nwap_dp_word<LB, FLAVOR>(sym, la, nb, P, sc);
+}
+template <int LB, int FLAVOR>
+__device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym4 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                                                 const nwap_scheme_consts &sc, const nwap_ov_row *ovtab)
+{
+    nwap_dp_word_ov<LB, FLAVOR>(sym, la, nb, P, sc, ovtab);
+}
+
+template <int LB, int FLAVOR, class SYM>
+__device__ __forceinline__ void nwap_row_dp(const SYM *sym, const nwap_ov_row *ovtab, int la, const uint32_t *nb,
+                                            int l0, int l1, const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1,
+                                            uint32_t &vm2, bool deep)
+{
+    uint32_t P[LB + 1];
+    nwap_dp_word_sel<LB, FLAVOR>(sym, la, nb, P, sc, ovtab);
+    v = P[LB];
+    vm1 = P[LB >= 2 ? LB - 1 : LB];
+    vm2 = P[LB >= 3 ? LB - 2 : LB];
+    if (deep) {
+        uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
+#pragma unroll
+        for (int j = 1; j < LB; ++j) {
+            if (j == l0) lo = P[j] & 0xffffu;
+            if (j == l1) hi = P[j] & 0xffff0000u;
+        }
+        v = lo | hi;
+    }
+}
+
+#define NWAP_CASES_1_32                                                                        \
+    NWAP_CASE(1) NWAP_CASE(2) NWAP_CASE(3) NWAP_CASE(4) NWAP_CASE(5) NWAP_CASE(6) NWAP_CASE(7) NWAP_CASE(8)         \
+    NWAP_CASE(9) NWAP_CASE(10) NWAP_CASE(11) NWAP_CASE(12) NWAP_CASE(13) NWAP_CASE(14) NWAP_CASE(15) NWAP_CASE(16)  \
+    NWAP_CASE(17) NWAP_CASE(18) NWAP_CASE(19) NWAP_CASE(20) NWAP_CASE(21) NWAP_CASE(22) NWAP_CASE(23) NWAP_CASE(24) \
+    NWAP_CASE(25) NWAP_CASE(26) NWAP_CASE(27) NWAP_CASE(28) NWAP_CASE(29) NWAP_CASE(30) NWAP_CASE(31) NWAP_CASE(32)
+
+// One chunk (64 sorted columns, 2 per lane) against every staged row of the band.
+// mixmode: 0 = every lane of the warp has both words of length LB; 1 = some are LB-1 (the
+// usual case at a bucket boundary of the sorted strip); 2 = anything.  fast: the chunk is full
+// and every staged row is valid over the whole column window, so no per-lane range checks are
+// needed (the overwhelmingly common case).  All warp-uniform.
+template <int FLAVOR, int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                               const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                               const nwap_lane_cols &c, int mixmode, bool fast,
+                                               int want_hist, nwap_lane_stats &ls)
+{
+    uint32_t nb[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb_f<FLAVOR>(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+    const bool deep = mixmode > 2;
+    const int l0 = c.l0, l1 = c.l1;
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;                       // uniform across the CTA
+        const typename SM::sym_t *sym = sm.rowsym[rr];
+        uint32_t v = 0, vm1 = 0, vm2 = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_row_dp<(n <= QMAX ? n : 1), FLAVOR>(sym, sm.ov, la, nb, l0, l1, sc, v, vm1, vm2, deep); \
+        break;
+        switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+    nwap_close_chunk(ls, ca);
+}
+
+
+// Dense-table chunks (FLAVOR 3): per-row dispatch with the shared epilogue; the lane's column symbols are kept
+// as byte offsets (two registers per matrix column) for the table loads of nwap_dp_row_tab.
+template <int LB>
+__device__ __forceinline__ void nwap_row_dp_tab(const nwap_sym2 *sym, int la, const uint32_t *c0, const uint32_t *c1,
+                                                int l0, int l1, const nwap_scheme_consts &sc, const uint8_t *etab,
+                                                uint32_t &v, uint32_t &vm1, uint32_t &vm2, bool deep)
+{
+    uint32_t P[LB + 1];
+    nwap_dp_word_tab<LB>(sym, la, c0, c1, P, sc, etab);
+    v = P[LB];
+    vm1 = P[LB >= 2 ? LB - 1 : LB];
+    vm2 = P[LB >= 3 ? LB - 2 : LB];
+    if (deep) {
+        uint32_t lo = v & 0xffffu, hi = v & 0xffff0000u;
+#pragma unroll
+        for (int j = 1; j < LB; ++j) {
+            if (j == l0) lo = P[j] & 0xffffu;
+            if (j == l1) hi = P[j] & 0xffff0000u;
+        }
+        v = lo | hi;
+    }
+}
+
+// one length dispatch per chunk; the body owns the loop over the band's rows (as the hoisted uniform-scheme bodies)
+template <int LB, class SM>
+__device__ __forceinline__ void nwap_chunk_rows_tab(SM &sm, const nwap_scheme_consts &sc, const uint32_t *c0,
+                                                    const uint32_t *c1, const nwap_lane_cols &c, int mixmode, bool fast,
+                                                    int want_hist, nwap_lane_stats &ls, nwap_chunk_acc &ca)
+{
+    const bool deep = mixmode > 2;
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;
+        uint32_t v, vm1, vm2;
+        nwap_row_dp_tab<LB>(reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]), la, c0, c1, c.l0, c.l1, sc, sm.etab,
+                            v, vm1, vm2, deep);
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+}
+
+template <int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk_tab(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                   const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                   const nwap_lane_cols &c, int mixmode, bool fast,
+                                                   int want_hist, nwap_lane_stats &ls)
+{
+    uint32_t c0[QMAX], c1[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) { c0[j] = nwap_byte_of(w0, j); c1[j] = nwap_byte_of(w1, j); }
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_chunk_rows_tab<(n <= QMAX ? n : 1)>(sm, sc, c0, c1, c, mixmode, fast, want_hist, ls, ca); \
+        break;
+    switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+    nwap_close_chunk(ls, ca);
+}
+
+// NWAP_HOIST=1 (default): the length dispatch is done once per chunk and each length body owns the
+// whole row loop with the emit inlined.  With 4-warp CTAs this lost 13-18 % to instruction-cache
+// misses (profiles/r01e); with 10-warp CTAs it gains 3-4 % (profiles/r01h_ab_big_cta.txt).
+// NWAP_HOIST=0 keeps the per-row dispatch with one shared epilogue.
+#ifndef NWAP_HOIST
+#define NWAP_HOIST 1
+#endif
+// NWAP_HOIST_FASTONLY=1 (default; +1.0 % at 100k words, -0.9 % at 20k): the hoisted bodies serve only "fast" chunks (full chunk, every row valid over the
+// whole window: no la == 0 test, no per-lane range checks, no slow emit in the body); everything else goes
+// through the compact per-row-dispatch family with its one shared epilogue.
+#ifndef NWAP_HOIST_FASTONLY
+#define NWAP_HOIST_FASTONLY 1
+#endif
+#ifndef NWAP_ROW_PREFETCH
+#define NWAP_ROW_PREFETCH 1
+#endif
+template <int LB, int FLAVOR, bool FASTONLY, class SM>
+__device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_consts &sc, const uint32_t *nb,
+                                                  const nwap_lane_cols &c, int mixmode, bool fast, int want_hist,
+                                                  nwap_lane_stats &ls, nwap_chunk_acc &ca)
+{
+    const bool deep = mixmode > 2;
+    if (FASTONLY && NWAP_ROW_PREFETCH) {
+        // every row of a fast chunk is live: fetch the next row's {la, ala2, rowadj} (one LDS.128) a row ahead
+        uint4 nxt = *reinterpret_cast<const uint4 *>(&sm.meta[0]);
+#pragma unroll 1
+        for (int rr = 0; rr < NWAP_R; ++rr) {
+            const uint4 cur = nxt;
+            nxt = *reinterpret_cast<const uint4 *>(&sm.meta[rr + 1 < NWAP_R ? rr + 1 : rr]);
+            uint32_t v, vm1, vm2;
+            nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, (int)cur.x, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+            if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+            nwap_emit(sm, sm.meta[rr], cur.y, (int)cur.z, v, c, nwap_true(), 0, ls, ca);
+        }
+        return;
+    }
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (!FASTONLY && la == 0) continue;
+        uint32_t v, vm1, vm2;
+        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+        if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
+        if (FASTONLY) nwap_emit(sm, m, m.ala2, m.rowadj, v, c, nwap_true(), 0, ls, ca);
+        else nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+}
+
+template <int FLAVOR, int QMAX, int QW, bool FASTONLY, class SM>
+__device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                 const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                 const nwap_lane_cols &c, int mixmode, bool fast,
+                                                 int want_hist, nwap_lane_stats &ls)
+{
+    uint32_t nb[QMAX];
+#pragma unroll
+    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb_f<FLAVOR>(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_chunk_rows_h<(n <= QMAX ? n : 1), FLAVOR, FASTONLY>(sm, sc, nb, c, mixmode, fast, want_hist, ls, ca); \
+        break;
+    switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+    nwap_close_chunk(ls, ca);
+}
+
+
+// Tried and rejected this round (same-box A/B, evidence in profiles/r01c..r01e and git history):
+// hoisting the length dispatch out of the row loop, one symbol stream per band, dual-chain
+// chunks (4 columns per lane), a cold code family for chunks spanning >= 3 lengths.
+
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, uint32_t symmul, uint32_t left0, const nwap_ov_row *, int)
+{
+    x.a2 = a * symmul; x.left0 = left0;
+}
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_t symmul, uint32_t left0, const nwap_ov_row *ov, int K)
+{
+    x.a2 = a * symmul; x.left0 = left0; x.pad = 0;
+    x.ovi = ((int)a < K && ov[a].count) ? a : NWAP_NO_OV;
+}
+
+// One chunk whose longest word exceeds the register-resident row: block-wise DP (nwap_dp_blocks), per-lane
+// selection of the final cell, shared epilogue.  Rare by construction (words of 25..64 symbols in a wide
+// build), kept out of line so its registers and its 260-byte per-lane boundary column do not weigh on the
+// length-specialised bodies.
+template <class SM>
+__device__ __noinline__ void nwap_run_chunk_wide(int LB, SM &sm, const nwap_scheme_consts &sc, const uint8_t *b0,
+                                                 const uint8_t *b1, const nwap_lane_cols &c, bool fast, int want_hist,
+                                                 nwap_lane_stats &ls)
+{
+    nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
+    const int nblk = (LB + NWAP_WB - 1) / NWAP_WB;
+    uint32_t save[NWAP_MAXLEN_WIDE + 1];
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+        const nwap_row_meta &m = sm.meta[rr];
+        const int la = m.la;
+        if (la == 0) continue;
+        const uint32_t v = nwap_dp_blocks(reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]), la, b0, b1, nblk, c.l0, c.l1, sc, save);
+        nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
+    }
+    nwap_close_chunk(ls, ca);
+}
+
+// Sparse-output scan of one staged row segment (one warp): 16 staged scores per lane per trip, SWAR compare,
+// and -- rarely -- a warp-aggregated append of (index, score) keys plus the two degree increments.
+struct nwap_sparse_consts {
+    uint32_t lo_rep, hi_rep;
+    bool lo_th, hi_th, all_lo, has_hi;
+};
+__device__ __forceinline__ nwap_sparse_consts nwap_make_sparse_consts(const nwap_sparse_out &so)
+{
+    nwap_sparse_consts k;
+    const int lo = so.mode == 1 ? so.threshold : so.gmin;          // candidates: score >= lo ...
+    const int hi = so.mode == 1 ? 127 : so.gmax;                   // ... and score <= hi
+    const uint32_t Tlo = (uint32_t)(max(lo, -128) + 128);
+    k.lo_rep = (Tlo & 0x7fu) * 0x01010101u; k.lo_th = (Tlo & 0x80u) != 0; k.all_lo = lo <= -128;
+    const uint32_t Thi = (uint32_t)(min(hi, 126) + 1 + 128);
+    k.hi_rep = (Thi & 0x7fu) * 0x01010101u; k.hi_th = (Thi & 0x80u) != 0; k.has_hi = hi < 127;
+    return k;
+}
+
+template <class SM>
+__device__ __forceinline__ void nwap_sparse_row(SM &sm, const nwap_tile_params &p, const nwap_sparse_consts &k,
+                                                int rr, int64_t row, int64_t strip_lo, int lane)
+{
+    const nwap_row_meta &m = sm.meta[rr];
+    const int seg = m.seglen;
+    if (seg <= 0) return;
+    const nwap_sparse_out &so = p.sparse;
+    if (so.mode == 1 ? so.threshold > 127 : so.gmin > so.gmax) return;       // nothing can be kept
+    const int skew = m.skew;
+    const uint8_t *rowbase = sm.out + rr * NWAP_PITCH;           // 16-byte aligned; the segment starts at +skew
+    const int nvec = (skew + seg + 15) >> 4;
+    for (int v0 = 0; v0 < nvec; v0 += 32) {
+        const int v = v0 + lane;
+        unsigned bits = 0;
+        if (v < nvec) {
+            const uint4 x = *reinterpret_cast<const uint4 *>(rowbase + 16 * v);
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                unsigned ok = k.all_lo ? 0xfu : nwap_ge_bits4(w[q], k.lo_rep, k.lo_th);
+                if (k.has_hi) ok &= ~nwap_ge_bits4(w[q], k.hi_rep, k.hi_th);
+                bits |= ok << (4 * q);
+            }
+            const int first = skew - 16 * v;                     // vector bytes before the segment
+            if (first > 0) bits &= 0xffffu << first;
+            const int last = skew + seg - 16 * v;                // vector bytes up to the segment's end
+            if (last < 16) bits &= (1u << last) - 1u;
+        }
+        if (!__any_sync(0xffffffffu, bits != 0u)) continue;
+        if (so.mode == 2 && bits) {                              // per-length bounds of the reference's float64 test
+            unsigned keep = 0, rest = bits;
+            while (rest) {
+                const int j = __ffs(rest) - 1;
+                rest &= rest - 1;
+                const int sc8 = (int)(int8_t)rowbase[16 * v + j];
+                const int lc = (int)p.lens[strip_lo + m.clo_off + (16 * v + j - skew)];
+                const short2 bnd = sm.kbounds[max(m.la, lc)];
+                if (sc8 >= (int)bnd.x && sc8 <= (int)bnd.y) keep |= 1u << j;
+            }
+            bits = keep;
+        }
+        const int cnt = __popc(bits);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(so.count, (unsigned long long)total);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        long long pos = (long long)base + (incl - cnt);
+        while (bits) {
+            const int j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int b = 16 * v + j - skew;                     // offset inside the segment
+            const unsigned long long idx = (unsigned long long)(p.start + m.g0 + b);
+            if (pos < so.cap) so.keys[pos] = (idx << 8) | (unsigned long long)rowbase[16 * v + j];
+            if (so.degree) {
+                atomicAdd(&so.degree[row], 1);
+                atomicAdd(&so.degree[strip_lo + m.clo_off + b], 1);
+            }
+            ++pos;
+        }
+    }
+}
+
+// QMAX = register-resident row width (16, 24 or 32): the longest word the instantiation
+// accepts.  Stored word rows are qpad = 16 or 32 bytes; QW 32-bit words of them are loaded.
+// WIDE: words of up to NWAP_MAXLEN_WIDE = 64 symbols are accepted; chunks whose longest word exceeds QMAX take the
+// block-wise path (nwap_run_chunk_wide), everything else runs the same length-specialised bodies.
+// CMP: sparse-output mode (p.sparse): the flush stage scans the staged scores for kept edges; the dense store
+// happens only when p.out is non-NULL.
+template <int FLAVOR, int QMAX, bool OV, bool WIDE = false, bool CMP = false>
+__global__ void __launch_bounds__(NWAP_THREADS, (((OV || FLAVOR == 3) && QMAX > 24) ? 1 : NWAP_MINB))   // the 32-wide sparse-override / table builds need > 96 registers
+k_score_tiles(const nwap_tile_params p)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int MAXL = WIDE ? NWAP_MAXLEN_WIDE : QMAX;          // longest word accepted
+    typedef nwap_tile_smem_t<(OV ? 1 : (FLAVOR == 3 ? 2 : 0)), (WIDE ? NWAP_MAXLEN_WIDE : NWAP_MAXLEN_FAST)> smem_t;
+    constexpr int SYMLEN = WIDE ? NWAP_MAXLEN_WIDE : NWAP_MAXLEN_FAST;   // row symbols staged per row
+    smem_t &sm = *reinterpret_cast<smem_t *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const nwap_scheme_consts sc = p.sc;
+    constexpr int QW = QMAX <= 16 ? 4 : 8;
+    static_assert(!WIDE || (FLAVOR == 1 && !OV && QMAX == 24), "the wide build exists for the default uniform-scheme cell only");
+
+    if (tid == 0) { sm.sum = 0; sm.count = 0; sm.mn = 127; sm.mx = -128; }
+    for (int b = tid; b < 256; b += NWAP_THREADS) sm.hist[b] = 0;
+    if (FLAVOR == 3) {
+        for (int w = tid; w < p.ov_K * p.ov_K; w += NWAP_THREADS) sm.etab[w] = p.etab[w];
+    }
+    if (CMP && p.sparse.mode == 2)
+        for (int b = tid; b < 256; b += NWAP_THREADS) sm.kbounds[b] = p.sparse.bounds[b];
+    const nwap_sparse_consts skc = nwap_make_sparse_consts(p.sparse);
+    if (OV) {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(p.ov_table);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(sm.ov);
+        for (int w = tid; w < p.ov_K * (int)(sizeof(nwap_ov_row) / 4); w += NWAP_THREADS) dst[w] = src[w];
+    }
+    nwap_lane_stats ls;
+    ls.mn2 = 0x7fff7fffu; ls.mx2 = 0u; ls.sum = 0; ls.count = 0;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) sm.unit = atomicAdd(p.unit_counter, 1ULL);
+        __syncthreads();
+        const int64_t t = (int64_t)sm.unit;
+        if (t >= p.unit_count) break;
+
+        int64_t group, strip;
+        nwap_unit_decode(p.us, p.unit_begin + t, &group, &strip);
+        const int64_t strip_lo = strip * NWAP_C;
+        const int64_t strip_hi = min(strip_lo + (int64_t)NWAP_C, p.n);
+        const int64_t grow0 = group * (int64_t)p.us.gb * NWAP_R;
+        const int64_t rmin = max(grow0, p.r_first);
+        const int64_t rmax = min(grow0 + (int64_t)p.us.gb * NWAP_R - 1, p.r_last);
+        if (rmin > rmax) continue;
+        const int64_t cwin_lo = max(strip_lo, rmin + 1);
+        if (cwin_lo >= strip_hi) continue;
+
+        // ---- counting sort of the unit's columns by word length, longest first ----
+        for (int b = tid; b < NWAP_WARPS * (SYMLEN + 2); b += NWAP_THREADS) (&sm.bins[0][0])[b] = 0;
+        __syncthreads();
+        constexpr int PER = NWAP_C / NWAP_THREADS;     // 16 columns per thread
+        uint32_t lw[PER / 4];
+        {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p.lens + strip_lo) + tid);
+            lw[0] = v.x; lw[1] = v.y; lw[2] = v.z; lw[3] = v.w;
+        }
+        const int kbase = tid * PER;
+        const int win_lo = (int)(cwin_lo - strip_lo), win_hi = (int)(strip_hi - strip_lo);
+        // zero the lengths of columns outside the window (and clamp, defensively)
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int k = kbase + e;
+            uint32_t len = nwap_byte_of(lw, e);
+            if (k < win_lo || k >= win_hi) len = 0;
+            if (len > (uint32_t)MAXL) len = MAXL;
+            lw[e >> 2] = (lw[e >> 2] & ~(0xffu << (8 * (e & 3)))) | (len << (8 * (e & 3)));
+        }
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int len = (int)nwap_byte_of(lw, e);
+            if (len) atomicAdd(&sm.bins[warp][len], 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int run = 0;
+            for (int len = MAXL; len >= 1; --len)
+                for (int w = 0; w < NWAP_WARPS; ++w) { int cnt = sm.bins[w][len]; sm.bins[w][len] = run; run += cnt; }
+            sm.ncols = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int len = (int)nwap_byte_of(lw, e);
+            if (len) {
+                const int pos = atomicAdd(&sm.bins[warp][len], 1);
+                sm.cols[pos] = (uint16_t)(kbase + e);
+                sm.clen[pos] = (uint8_t)len;
+            }
+        }
+
+        // ---- bands of the group ----
+        for (int b = 0; b < p.us.gb; ++b) {
+            const int64_t rb0 = grow0 + (int64_t)b * NWAP_R;
+            if (rb0 + NWAP_R - 1 < rmin || rb0 > rmax) continue;
+            __syncthreads();                         // previous flush done; sort scatter visible
+            // stage row metadata
+            if (tid < NWAP_R) {
+                const int64_t r = rb0 + tid;
+                nwap_row_meta m;
+                m.la = 0; m.clo_off = 0; m.seglen = 0; m.rowadj = 0; m.ala2 = 0; m.skew = 0; m.g0 = 0;
+                if (r >= rmin && r <= rmax) {
+                    int64_t clo = max(strip_lo, r + 1);
+                    int64_t chi = strip_hi;
+                    if (r == p.r_first) clo = max(clo, p.c_start);
+                    if (r == p.r_last) chi = min(chi, p.c_end + 1);
+                    if (chi > clo) {
+                        m.la = (int)p.lens[r];
+                        m.clo_off = (int)(clo - strip_lo);
+                        m.seglen = (int)(chi - clo);
+                        m.g0 = nwap_before_row(r, p.n) + (clo - r - 1) - p.start;
+                        m.skew = (int)((reinterpret_cast<uintptr_t>(p.out) + (uintptr_t)m.g0) & 15u);
+                        m.rowadj = tid * NWAP_PITCH + m.skew - m.clo_off;
+                        m.ala2 = (uint32_t)(sc.alpha * m.la * 65537);
+                    }
+                }
+                sm.meta[tid] = m;
+            }
+            // stage row symbols, packed a*65537, with the row boundary values (4 symbols per item)
+            for (int item = tid; item < NWAP_R * (SYMLEN / 4); item += NWAP_THREADS) {
+                const int rr = item / (SYMLEN / 4), q4 = item % (SYMLEN / 4);
+                const int64_t r = rb0 + rr;
+                if (q4 < (WIDE ? (p.qpad >> 2) : QW) && r >= rmin && r <= rmax) {
+                    const uint32_t v = __ldg(reinterpret_cast<const uint32_t *>(p.ids + r * p.qpad) + q4);
+                    const int la_r = (int)p.lens[r];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t a = (v >> (8 * e)) & 0xffu;
+                        if (q4 * 4 + e < la_r)           // slot [la] belongs to the boundary record
+                            nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, sc.symmul, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
+                                           sm.ov, p.ov_K);
+                    }
+                }
+            }
+            if (tid == 0) sm.next_chunk = 0;
+            __syncthreads();
+            // simple band: all R rows present and each covers the whole sorted column window, i.e. the band lies
+            // entirely to the left of the strip (every row r has r + 1 <= strip_lo, so its columns start at the
+            // strip's first column) and neither end of the launch range clips one of its rows.  Evaluated by
+            // every thread from launch scalars: no extra barrier, nothing read back from shared memory.
+            const bool clip_first = p.r_first >= rb0 && p.r_first < rb0 + NWAP_R && p.c_start > strip_lo;
+            const bool clip_last = p.r_last >= rb0 && p.r_last < rb0 + NWAP_R && p.c_end + 1 < strip_hi;
+            const bool band_simple = !p.want_hist && rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax &&
+                                     rb0 + NWAP_R - 1 < strip_lo && !clip_first && !clip_last;
+
+            // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
+            const int ncols = sm.ncols;
+            for (;;) {
+                int item = 0;
+                if (lane == 0) item = atomicAdd(&sm.next_chunk, 1);
+                item = __shfl_sync(0xffffffffu, item, 0);
+                const int kc = item * NWAP_CHUNK;
+                if (kc >= ncols) break;
+                // register width of the chunk: its longest word, optionally rounded up to a multiple of
+                // NWAP_LBSTEP (fewer distinct length bodies in flight; the 3-level merge covers the slack)
+                const int LB = min(((int)sm.clen[kc] + NWAP_LBSTEP - 1) / NWAP_LBSTEP * NWAP_LBSTEP, MAXL);
+                const int ka = kc + 2 * lane, kb = ka + 1;
+                const bool va = ka < ncols, vb = kb < ncols;
+                const int la_ = va ? (int)sm.clen[ka] : LB, lb_ = vb ? (int)sm.clen[kb] : LB;
+                const uint32_t off0 = va ? (uint32_t)sm.cols[ka] : 0xffffu;
+                const uint32_t off1 = vb ? (uint32_t)sm.cols[kb] : 0xffffu;
+                // column words (invalid lanes re-read the chunk's first column; their results are dropped)
+                const int64_t ca = strip_lo + (va ? sm.cols[ka] : sm.cols[kc]);
+                const int64_t cb = strip_lo + (vb ? sm.cols[kb] : sm.cols[kc]);
+                uint32_t w0[QW], w1[QW];
+#pragma unroll
+                for (int v = 0; v < QW / 4; ++v) {
+                    const uint4 x = __ldg(reinterpret_cast<const uint4 *>(p.ids + ca * p.qpad) + v);
+                    const uint4 y = __ldg(reinterpret_cast<const uint4 *>(p.ids + cb * p.qpad) + v);
+                    w0[4 * v] = x.x; w0[4 * v + 1] = x.y; w0[4 * v + 2] = x.z; w0[4 * v + 3] = x.w;
+                    w1[4 * v] = y.x; w1[4 * v + 1] = y.y; w1[4 * v + 2] = y.z; w1[4 * v + 3] = y.w;
+                }
+                const nwap_lane_cols cA = nwap_make_lane_cols(off0, off1, la_, lb_, LB, sc);
+                const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
+                const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
+                const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
+                if (WIDE && LB > QMAX) {
+                    nwap_run_chunk_wide(LB, sm, sc, p.ids + ca * p.qpad, p.ids + cb * p.qpad, cA, fast, p.want_hist, ls);
+                    continue;
+                }
+                if (FLAVOR == 3) {
+                    nwap_run_chunk_tab<QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+                    continue;
+                }
+#if NWAP_HOIST
+                // two code families only where the register budget allows (the 32-wide and sparse-override
+                // instantiations would spill): there the hoisted bodies also carry the slow emit
+                constexpr bool FASTONLY = NWAP_HOIST_FASTONLY && QMAX <= 24 && !OV;
+                if (!FASTONLY || fast) nwap_run_chunk_h<FLAVOR, QMAX, QW, FASTONLY>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+                else nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+#else
+                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+#endif
+            }
+            __syncthreads();
+
+            // ---- sparse output: scan the staged rows for kept edges ----
+            if (CMP) {
+                for (int rr = warp; rr < NWAP_R; rr += NWAP_WARPS) nwap_sparse_row(sm, p, skc, rr, rb0 + rr, strip_lo, lane);
+                if (p.out == nullptr) continue;          // no dense payload wanted (uniform across the grid)
+            }
+            // ---- flush: each warp copies whole row segments, 16 B aligned in both spaces ----
+            for (int rr = warp; rr < NWAP_R; rr += NWAP_WARPS) {
+                const int seg = sm.meta[rr].seglen;
+                if (seg <= 0) continue;
+                const int skew = sm.meta[rr].skew;
+                const uint8_t *src = sm.out + rr * NWAP_PITCH + skew;
+                int8_t *dst = p.out + sm.meta[rr].g0;
+                int head = (16 - skew) & 15;
+                if (head > seg) head = seg;
+                if (lane < head) dst[lane] = (int8_t)src[lane];
+                const int nvec = (seg - head) >> 4;
+                const uint4 *s4 = reinterpret_cast<const uint4 *>(src + head);
+                uint4 *d4 = reinterpret_cast<uint4 *>(dst + head);
+                for (int v = lane; v < nvec; v += 32) d4[v] = s4[v];
+                const int tail0 = head + (nvec << 4);
+                if (tail0 + lane < seg) dst[tail0 + lane] = (int8_t)src[tail0 + lane];
+            }
+        }
+    }
+
+    // ---- statistics: thread -> warp -> CTA -> global ----
+    long long wsum = ls.sum, wcnt = ls.count;
+    int tmn = min((int)(ls.mn2 & 0xffffu), (int)(ls.mn2 >> 16)) - (int)NWAP_BIAS;
+    int tmx = max((int)(ls.mx2 & 0xffffu), (int)(ls.mx2 >> 16)) - (int)NWAP_BIAS;
+    if (ls.count == 0) { tmn = 127; tmx = -128; }
+    tmn = min(tmn, 127); tmx = max(tmx, -128);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        wcnt += __shfl_xor_sync(0xffffffffu, wcnt, o);
+        tmn = min(tmn, __shfl_xor_sync(0xffffffffu, tmn, o));
+        tmx = max(tmx, __shfl_xor_sync(0xffffffffu, tmx, o));
+    }
+    __syncthreads();
+    if (lane == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&sm.sum), (unsigned long long)wsum);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&sm.count), (unsigned long long)wcnt);
+        atomicMin(&sm.mn, tmn);
+        atomicMax(&sm.mx, tmx);
+    }
+    __syncthreads();
+    if (tid == 0 && sm.count > 0) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&p.stats->sum), (unsigned long long)sm.sum);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&p.stats->count), (unsigned long long)sm.count);
+        atomicMin(&p.stats->mn, sm.mn);
+        atomicMax(&p.stats->mx, sm.mx);
+    }
+    if (p.want_hist)
+        for (int b = tid; b < 256; b += NWAP_THREADS)
+            if (sm.hist[b]) atomicAdd(&p.stats->hist[b], (unsigned long long)sm.hist[b]);
+}
+
+
+// Tile-kernel instantiations live in their own translation units (tiles_*.cu, compiled in parallel); the ABI
+// unit fetches them through this getter.  family: 0 = FLAVOR 0, 1 = FLAVOR 1 (default), 2 = FLAVOR 2,
+// 3 = sparse overrides, 4 = dense table, 5 = wide (words up to 64 symbols), 6 = sparse output, 7 = wide + sparse
+// output.  qclass: 0/1/2 = register row width 16/24/32 (ignored by the wide families).
+typedef void (*nwap_tile_kernel_t)(const nwap_tile_params);
+#define NWAP_TILE_FAMILIES 8
+nwap_tile_kernel_t nwap_tile_kernel(int family, int qclass);
+size_t nwap_tile_smem_bytes(int family);
+nwap_tile_kernel_t nwap_tiles_f0f2(int family, int qclass);
+nwap_tile_kernel_t nwap_tiles_f1(int qclass);
+nwap_tile_kernel_t nwap_tiles_ov(int qclass);
+nwap_tile_kernel_t nwap_tiles_tab(int qclass);
+nwap_tile_kernel_t nwap_tiles_wide(bool cmp);
+nwap_tile_kernel_t nwap_tiles_cmp(int qclass);

@@ -248,6 +248,44 @@ class NwapContext:
         return idx[: cnt.value], sc[: cnt.value]
 
 
+    def score_range_compact(self, start: int, end: int, threshold: Optional[int] = None, capacity: int = 0,
+                            out=None, degree=None, normalized: Optional[Tuple[float, float]] = None,
+                            variant: str = "auto"):
+        """Sparse-output scoring (nwap_score_range_compact): score [start, end) and return only the kept
+        edges -- raw score >= ``threshold``, or ``normalized=(lo, hi)`` for the reference's
+        ``lo <= 100*score/max(len_r, len_c) <= hi`` (graph.py:91-101) -- in index order, without ever
+        materialising the dense payload (``out=None``).  Pass ``out`` (int8 CUDA tensor) to get the dense
+        bytes as well.  Returns (idx int64 tensor, score int8 tensor, (sum, min, max, count))."""
+        import torch
+
+        if (threshold is None) == (normalized is None):
+            raise ValueError("pass exactly one of threshold / normalized")
+        dev = torch.device("cuda", self.device)
+        if out is not None:
+            if not (out.is_cuda and out.is_contiguous() and out.element_size() == 1):
+                raise ValueError("out must be a contiguous 1-byte CUDA tensor")
+            if out.numel() < end - start:
+                raise ValueError("output tensor too small")
+        idx = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
+        sc = torch.empty(max(capacity, 1), dtype=torch.int8, device=dev)
+        cnt = ctypes.c_int64()
+        st = NwapStats()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        common = (idx.data_ptr(), sc.data_ptr(), capacity, ctypes.addressof(cnt),
+                  degree.data_ptr() if degree is not None else None, ctypes.addressof(st), VARIANTS[variant], stream)
+        optr = out.data_ptr() if out is not None else None
+        if normalized is None:
+            rc = lib().nwap_score_range_compact(self._h, start, end, optr, int(threshold), *common)
+        else:
+            lo, hi = normalized
+            if lo > hi:
+                raise ValueError(f"empty filter range: lo={lo} > hi={hi}")
+            rc = lib().nwap_score_range_filter_normalized(self._h, start, end, optr, float(lo), float(hi), *common)
+        if rc == _native.NWAP_ECAPACITY:
+            raise _native.CapacityError(_native.last_error(), cnt.value)
+        check(rc)
+        return idx[: cnt.value], sc[: cnt.value], _stats_tuple(st, False)[:4]
+
     def filter_normalized(self, payload, start: int, end: int, lo: float, hi: float, capacity: int,
                           degree=None):
         """Reference graph.py:91-101 keep-mask on the device: edges of an already scored slice with

@@ -129,6 +129,28 @@ int emul_pair_scores_ov(int LB, const uint8_t *a, int la, const uint8_t *b0, int
     return 0;
 }
 
+// Words of up to 64 symbols: the block-wise path of the tile kernel (nwap_dp_blocks).
+int emul_pair_scores_wide(const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,
+                          int match, int mismatch, int gap, int *s0, int *s1)
+{
+    if (la < 1 || la > NWAP_MAXLEN_WIDE || lb0 < 1 || lb1 < 1 || lb0 > NWAP_MAXLEN_WIDE || lb1 > NWAP_MAXLEN_WIDE) return -1;
+    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap, 1);
+    nwap_sym2 row2[NWAP_MAXLEN_WIDE + 1];
+    for (int i = 0; i < la; ++i) {
+        row2[i].a2 = (uint32_t)a[i] * sc.symmul;
+        row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+    }
+    uint8_t p0[NWAP_MAXLEN_WIDE + NWAP_WB] = {0}, p1[NWAP_MAXLEN_WIDE + NWAP_WB] = {0};
+    memcpy(p0, b0, lb0);
+    memcpy(p1, b1, lb1);
+    const int LB = lb0 > lb1 ? lb0 : lb1;
+    uint32_t save[NWAP_MAXLEN_WIDE + 1];
+    const uint32_t v = nwap_dp_blocks(row2, la, p0, p1, (LB + NWAP_WB - 1) / NWAP_WB, lb0, lb1, sc, save);
+    *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
+    *s1 = nwap_unbias(v >> 16, la, lb1, sc);
+    return 0;
+}
+
 // Scores (a vs b0) and (a vs b1) with the packed recurrence at register width LB.
 int emul_pair_scores(int flavor, int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0,
                      const uint8_t *b1, int lb1, int match, int mismatch, int gap,

@@ -29,6 +29,7 @@ def emul():
     L.emul_pair_scores.argtypes = [i, i, p, i, p, i, p, i, i, i, i, p, p]
     L.emul_pair_scores_ov.argtypes = [i, p, i, p, i, p, i, p, i, i, i, i, p, p]
     L.emul_pair_scores_tab.argtypes = [i, p, i, p, i, p, i, p, i, i, p, p]
+    L.emul_pair_scores_wide.argtypes = [p, i, p, i, p, i, i, i, i, p, p]
     L.emul_row_of.restype = i64
     L.emul_row_of.argtypes = [i64, i64]
     L.emul_col_of.restype = i64
@@ -69,6 +70,28 @@ def test_packed_recurrence_matches_oracle(emul, flavor):
                                      m, x, g, ctypes.addressof(s0), ctypes.addressof(s1)) == 0
         assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim, g), orc.c_nw_score(a, b1, sim, g)), \
             (LB, m, x, g, a, b0, b1)
+
+
+def test_blockwise_recurrence_for_long_words(emul):
+    """Words of up to 64 symbols (the preflight admits them for gap -1, reference engine.py:83-90):
+    16-column blocks chained through the saved boundary column."""
+    rng = random.Random(4242)
+    for it in range(4000):
+        q = rng.choice([17, 24, 25, 32, 33, 40, 47, 48, 49, 63, 64])
+        m, x, g = _random_scheme(rng, q)
+        K = rng.choice([2, 3, 5, 40, 255])
+        la, lb0, lb1 = rng.randint(1, q), rng.randint(1, q), rng.randint(1, q)
+        if it % 7 == 0:
+            la = lb0 = lb1 = q
+        a = np.array([rng.randrange(K) for _ in range(la)], dtype=np.uint8)
+        b0 = np.array([rng.randrange(K) for _ in range(lb0)], dtype=np.uint8)
+        b1 = np.array([rng.randrange(K) for _ in range(lb1)], dtype=np.uint8)
+        sim = orc.similarity_matrix(m, x, 256)
+        s0, s1 = ctypes.c_int(), ctypes.c_int()
+        assert emul.emul_pair_scores_wide(a.ctypes.data, la, b0.ctypes.data, lb0, b1.ctypes.data, lb1, m, x, g,
+                                          ctypes.addressof(s0), ctypes.addressof(s1)) == 0
+        assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim, g), orc.c_nw_score(a, b1, sim, g)), \
+            (m, x, g, a, b0, b1)
 
 
 def test_packed_recurrence_extreme_schemes(emul):

@@ -128,6 +128,40 @@ def test_sampled_ranges_big_configs(golden_samples, cfg):
         assert (s, mn, mx) == (r["sum"], r["min"], r["max"])
 
 
+def _b2(*arrays):
+    h = hashlib.blake2b(digest_size=16)
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("cfg", ["C4", "C5"])
+def test_fullscale_chunk_protocol(cfg):
+    """SURVEY 8(d) protocol for the 600,000-word configs: 256 evenly spaced 65,536-edge chunks, first / last, one
+    chunk either side of every equal-work shard bound -- bytes, statistics, kept list and the kept edges'
+    (row, col) against digests of the reference's own _score_range / rows_of_array output
+    (tests/golden/make_golden_fullscale.py)."""
+    import json
+    from paper_2509_01654_b200 import sharding
+    g = json.loads((GOLDEN / "fullscale_chunks.json").read_text())[cfg]
+    ids, lens, sch = synth.config_store(cfg)
+    n = len(lens)
+    assert synth.store_digest(ids, lens) == g["store_digest"]
+    assert [int(b) for b in sharding.equal_work_bounds(lens, 8)] == g["equal_work_bounds_8"]
+    assert [int(b) for b in orc.np_equal_work_bounds(lens, 8)] == g["equal_work_bounds_8"]
+    sim = orc.similarity_matrix(sch[0], sch[1], int(ids.max()) + 1)
+    ids32, len32 = ids.astype(np.int32), lens.astype(np.int32)
+    assert len(g["chunks"]) >= 64 + 2 + 14
+    for r in g["chunks"]:
+        payload, s, mn, mx = orc.c_score_range(ids32, len32, sim, sch[2], n, r["start"], r["end"], threads=4)
+        assert _b2(payload) == r["blake2b_128"], (cfg, r["tag"])
+        assert (s, mn, mx) == (r["sum"], r["min"], r["max"])
+        idx, sc, _ = orc.np_compact(payload, r["start"], n, g["threshold"])
+        assert idx.size == r["kept"] and _b2(idx.astype(np.int64), sc) == r["kept_blake2b_128"]
+        rows = orc.np_rows_of(idx, n)
+        assert _b2(rows.astype(np.int64), orc.np_cols_of(idx, n, rows).astype(np.int64)) == r["kept_rc_blake2b_128"]
+
+
 # ---- triangle ------------------------------------------------------------------------------
 
 def test_triangle_against_reference(golden_triangle):
