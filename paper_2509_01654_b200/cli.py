@@ -5,10 +5,10 @@
 takes the reference's ``phonsim compute`` arguments (cli.py:75-85), prints the same four lines
 (cli.py:184-190), writes the same ``.nwedges`` + manifest files and uses the same exit codes
 (cli.py:13: 0 success, 1 usage error, 2 data error, 3 I/O error).  ``--workers`` is accepted and
-ignored; ``--device`` picks the GPU, ``--devices 0,1,...`` shares the edge range between several.  Scheme files (``--scheme``,
-parsed by aligner.py:195-239) belong to the reference's text front end and are not re-implemented:
-pass overrides through the Python API instead.  Every other ``phonsim`` sub-command works on the
-finished store and stays with the reference.
+ignored; ``--device`` picks the GPU, ``--devices 0,1,...`` shares the edge range between several.
+``--scheme FILE`` (aligner.py:195-239) with per-pair overrides resolved against ``--inventory`` -- or, as in the
+reference (cli.py:167-174), the ``.inventory`` file next to a ``.words`` file -- runs on the packed kernel's
+table-driven cell.  Every other ``phonsim`` sub-command works on the finished store and stays with the reference.
 """
 from __future__ import annotations
 
@@ -17,7 +17,9 @@ import sys
 
 from .engine import compute_all_pairs, preflight_range_check
 from .host_types import DEFAULT_CHUNK_SIZE, ComputePlan, DataError, ScoringScheme
-from .store import PipelinedEdgeStoreWriter, load_words
+import os
+
+from .store import PipelinedEdgeStoreWriter, load_inventory, load_scheme_file, load_words
 
 EXIT_OK, EXIT_USAGE, EXIT_DATA, EXIT_IO = 0, 1, 2, 3
 
@@ -39,8 +41,8 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--match", type=int, default=1)
     p.add_argument("--mismatch", type=int, default=-1)
     p.add_argument("--gap", type=int, default=-1)
-    p.add_argument("--scheme", default=None, help="not supported here (see module docstring)")
-    p.add_argument("--inventory", default=None, help="accepted for compatibility")
+    p.add_argument("--scheme", default=None, help="scheme file (match/mismatch/gap + per-pair overrides); overrides --match/--mismatch/--gap")
+    p.add_argument("--inventory", default=None, help="inventory sidecar for scheme-file overrides (default: <words_file stem>.inventory)")
     p.add_argument("--workers", type=int, default=1, help="accepted for compatibility, ignored")
     p.add_argument("--chunk-size", type=int, default=DEFAULT_CHUNK_SIZE)
     p.add_argument("--device", type=int, default=0, help="CUDA device index")
@@ -55,15 +57,20 @@ def cmd_compute(args) -> int:
         raise UsageError("workers must be positive")
     if args.chunk_size < 1:
         raise UsageError("chunk-size must be positive")
-    if args.scheme:
-        raise UsageError("scheme files are not supported by the GPU front end; use --match/--mismatch/--gap "
-                         "or the Python API (ScoringScheme(overrides=...))")
     try:
         devices = [int(d) for d in args.devices.split(",")] if args.devices else [args.device]
     except ValueError:
         raise UsageError("devices must be a comma-separated list of integers") from None
     words = load_words(args.words_file)
-    scheme = ScoringScheme(args.match, args.mismatch, args.gap)
+    if args.scheme:
+        inventory_path = args.inventory
+        if inventory_path is None and args.words_file.endswith(".words"):
+            guess = args.words_file[: -len(".words")] + ".inventory"
+            if os.path.exists(guess):
+                inventory_path = guess
+        scheme = load_scheme_file(args.scheme, load_inventory(inventory_path) if inventory_path else None)
+    else:
+        scheme = ScoringScheme(args.match, args.mismatch, args.gap)
     preflight_range_check(words, scheme)            # fail before any output file exists (cli.py:177)
     plan = ComputePlan(n=len(words), chunk_size=args.chunk_size, worker_count=args.workers, scheme=scheme)
     writer = PipelinedEdgeStoreWriter(args.out, words, scheme)
@@ -89,7 +96,7 @@ def main(argv=None) -> int:
     except ValueError as exc:
         print(f"usage error: {exc}", file=sys.stderr)
         return EXIT_USAGE
-    except OSError as exc:
+    except (OSError, RuntimeError, MemoryError) as exc:      # I/O and CUDA / device failures
         print(f"error: {exc}", file=sys.stderr)
         return EXIT_IO
 

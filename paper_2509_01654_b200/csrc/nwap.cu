@@ -106,6 +106,7 @@ struct nwap_ctx {
     uint8_t *d_etab = nullptr;
     std::vector<uint8_t> h_lens;        // host copy for shard arithmetic
     std::vector<int64_t> h_lenprefix;   // prefix sums of lengths (n+1)
+    std::vector<int64_t> h_rowpref;     // h_rowpref[r] = DP cells of rows < r (n+1)
     uint8_t *d_ids = nullptr;
     uint8_t *d_lens = nullptr;          // padded with zeros to a whole number of strips
     int8_t *d_sim = nullptr;            // K x K
@@ -354,6 +355,15 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     nwap_tile_kernel(family, qclass)<<<(unsigned)grid, NWAP_THREADS, nwap_tile_smem_bytes(family), st>>>(p);
     g_launches++;
     CK(cudaGetLastError());
+    if (want_hist && out_dev) {
+        // the histogram comes from a streaming pass over the bytes just written (still L2-warm for slabs): the
+        // scoring kernel keeps its fast emit, and the pass runs at 5.5 TB/s (profiles/r01_consumers_ncu.txt)
+        const int64_t count = end - start;
+        const int64_t blocks = std::min<int64_t>((count / 16 + 255) / 256 + 1, (int64_t)c->sm_count * 8);
+        k_payload_stats<<<(unsigned)blocks, 256, 0, st>>>(out_dev, count, c->d_stats, 1);
+        g_launches++;
+        CK(cudaGetLastError());
+    }
     return NWAP_OK;
 }
 
@@ -419,6 +429,9 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
     c->h_lenprefix.resize(n + 1);
     c->h_lenprefix[0] = 0;
     for (int64_t i = 0; i < n; ++i) c->h_lenprefix[i + 1] = c->h_lenprefix[i] + lengths[i];
+    c->h_rowpref.assign(n + 1, 0);
+    for (int64_t r = 0; r < n; ++r)
+        c->h_rowpref[r + 1] = c->h_rowpref[r] + (int64_t)lengths[r] * (c->h_lenprefix[n] - c->h_lenprefix[r + 1]);
 
     // repack rows to qpad on the host, then one H2D copy
     std::vector<uint8_t> packed((size_t)n * c->qpad, 0);
@@ -533,16 +546,11 @@ static int64_t cells_before(const nwap_ctx *c, int64_t idx)
 {
     const int64_t n = c->n, P = n * (n - 1) / 2;
     if (idx <= 0) return 0;
+    if (idx >= P) return c->h_rowpref[n - 1];
     const std::vector<int64_t> &pre = c->h_lenprefix;
-    auto row_cells_before = [&](int64_t r) {   // work of rows < r, O(r): cached below
-        int64_t w = 0;
-        for (int64_t k = 0; k < r; ++k) w += (int64_t)c->h_lens[k] * (pre[n] - pre[k + 1]);
-        return w;
-    };
-    if (idx >= P) return row_cells_before(n - 1);
     const int64_t r = nwap_row_of(idx, n);
     const int64_t col = nwap_col_of(idx, n, r);
-    return row_cells_before(r) + (int64_t)c->h_lens[r] * (pre[col] - pre[r + 1]);
+    return c->h_rowpref[r] + (int64_t)c->h_lens[r] * (pre[col] - pre[r + 1]);
 }
 
 int64_t nwap_cells_in_range(const nwap_ctx *c, int64_t start, int64_t end)
@@ -644,7 +652,7 @@ int nwap_payload_stats(nwap_ctx *c, const int8_t *payload_dev, int64_t count, nw
     if (rc) return rc;
     if (count > 0) {
         int64_t blocks = std::min<int64_t>((count / 16 + 255) / 256 + 1, (int64_t)c->sm_count * 8);
-        k_payload_stats<<<(unsigned)blocks, 256, 0, st>>>(payload_dev, count, c->d_stats);
+        k_payload_stats<<<(unsigned)blocks, 256, 0, st>>>(payload_dev, count, c->d_stats, 0);
         g_launches++;
         CK(cudaGetLastError());
     }
@@ -700,7 +708,7 @@ int nwap_compact_range(nwap_ctx *c, const int8_t *payload_dev, int64_t start, in
 {
     if (!c) return fail(NWAP_EINVAL, "null context");
     nwap_keep_params kp;
-    kp.threshold = threshold; memset(kp.smin, 0, sizeof kp.smin); memset(kp.smax, 0, sizeof kp.smax); kp.gmin = 0; kp.gmax = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    memset(&kp, 0, sizeof kp); kp.threshold = threshold; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
     return compact_common(c, payload_dev, start, end, 0, kp, idx_out_dev, score_out_dev, cap, count_host, degree_dev,
                           (cudaStream_t)stream);
 }
@@ -815,7 +823,7 @@ int nwap_filter_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start
     if (lo > hi) return fail(NWAP_EINVAL, "empty filter range: lo=%g > hi=%g", lo, hi);
     nwap_keep_params kp;
     kp.threshold = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
-    nwap_fill_norm_bounds(kp, lo, hi);
+    nwap_fill_norm_bounds(kp, lo, hi, c->qmax);
     return compact_common(c, payload_dev, start, end, 1, kp, idx_out_dev, score_out_dev, cap, count_host, degree_dev,
                           (cudaStream_t)stream);
 }
@@ -832,10 +840,21 @@ int nwap_hist_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, 
     ON_DEVICE(c->device);
     cudaStream_t st = (cudaStream_t)stream;
     nwap_keep_params kp;
-    kp.threshold = 0; memset(kp.smin, 0, sizeof kp.smin); memset(kp.smax, 0, sizeof kp.smax); kp.gmin = 0; kp.gmax = 0; kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    memset(&kp, 0, sizeof kp); kp.lens = c->d_lens; kp.n = c->n; kp.start = start;
+    const int64_t runs = (count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
+    if (c->qmax <= 100) {
+        // joint (max length, score) bins: no per-edge division, 26 KB of shared memory at 24 symbols
+        const size_t smem = sizeof(unsigned int) * 256 * (size_t)(c->qmax + 1);
+        CK(cudaFuncSetAttribute(k_hist_norm_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / (smem + 1024)));
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((runs + 511) / 512, (int64_t)c->sm_count * per_sm));
+        k_hist_norm_joint<<<(unsigned)blocks, 512, smem, st>>>(payload_dev, count, kp, (unsigned long long *)counts_dev, c->qmax);
+        g_launches++;
+        CK(cudaGetLastError());
+        return NWAP_OK;
+    }
     const size_t smem = sizeof(unsigned int) * NWAP_NHIST_SPAN;
     CK(cudaFuncSetAttribute(k_hist_normalized, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t runs = (count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((runs + 511) / 512, (int64_t)c->sm_count * 2));
     k_hist_normalized<<<(unsigned)blocks, 512, smem, st>>>(payload_dev, count, kp, (unsigned long long *)counts_dev);
     g_launches++;
@@ -848,9 +867,7 @@ int nwap_equal_work_bounds(const nwap_ctx *c, int parts, int64_t *bounds_out)
     if (!c || !bounds_out || parts < 1) return fail(NWAP_EINVAL, "bad argument");
     const int64_t n = c->n, P = n * (n - 1) / 2;
     const std::vector<int64_t> &pre = c->h_lenprefix;
-    // rowpref[r] = cells in rows < r
-    std::vector<int64_t> rowpref(n + 1, 0);
-    for (int64_t r = 0; r < n; ++r) rowpref[r + 1] = rowpref[r] + (int64_t)c->h_lens[r] * (pre[n] - pre[r + 1]);
+    const std::vector<int64_t> &rowpref = c->h_rowpref;      // rowpref[r] = cells in rows < r
     const __int128 W = rowpref[n];
     bounds_out[0] = 0;
     for (int g = 1; g < parts; ++g) {

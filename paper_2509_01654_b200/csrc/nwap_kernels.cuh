@@ -101,8 +101,9 @@ __global__ void k_init_stats(nwap_dev_stats *s, unsigned long long *counter)
 // Dense payload -> statistics (HBM-bound: 1 byte read per edge).  The loop only feeds the 256-bin histogram
 // (one shared-memory atomic per edge); sum, minimum and maximum are derived from the CTA's histogram at the end
 // (thread t owns bin t, value t - 128), so the per-edge work is an extract and an atomic.
+// hist_only: add the histogram only (the caller already holds sum / min / max / count from the scoring kernel).
 __global__ void __launch_bounds__(256)
-k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stats *stats)
+k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stats *stats, int hist_only)
 {
     __shared__ unsigned int shist[256];
     __shared__ long long ssum;
@@ -146,7 +147,7 @@ k_payload_stats(const int8_t *__restrict__ payload, int64_t count, nwap_dev_stat
     }
     if (h) atomicAdd(&stats->hist[tid], (unsigned long long)h);
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && !hist_only) {
         atomicAdd(reinterpret_cast<unsigned long long *>(&stats->sum), (unsigned long long)ssum);
         atomicMin(&stats->mn, smn);
         atomicMax(&stats->mx, smx);
@@ -203,10 +204,35 @@ __device__ __forceinline__ void nwap_load_lens64(const uint8_t *__restrict__ len
     }
 }
 
+// Rows of a compaction block (16 KiB of consecutive edges): almost always one or two, so one thread recovers
+// the first row (fp64 estimate + integer fix-up) and everyone else places itself by two comparisons.
+struct nwap_block_rows {
+    long long r0;          // row of the block's first live edge (-1: block holds no live edge)
+    long long next1;       // edge offset (relative to payload[0]) at which row r0 + 1 begins
+    long long next2;       // ... and row r0 + 2
+};
+
+__device__ __forceinline__ void nwap_block_rows_init(nwap_block_rows *br, const nwap_keep_params &kp, int64_t k_block,
+                                                     int64_t count)
+{
+    if (threadIdx.x == 0) {
+        const int64_t kb = max(k_block, (int64_t)0);
+        br->r0 = -1; br->next1 = br->next2 = 0;
+        if (kb < count) {
+            const int64_t r = nwap_row_of(kp.start + kb, kp.n);
+            br->r0 = r;
+            br->next1 = nwap_before_row(r + 1, kp.n) - kp.start;
+            br->next2 = nwap_before_row(min(r + 2, kp.n - 1), kp.n) - kp.start;
+        }
+    }
+}
+
 template <int MODE>
 __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__restrict__ payload, int64_t count,
                                                              int64_t k_first, const nwap_keep_params &kp,
-                                                             uint4 (&vec)[NWAP_CMP_VEC], const short2 *bounds)
+                                                             uint4 (&vec)[NWAP_CMP_VEC], const short2 *bounds,
+                                                             const short2 *rbounds = nullptr,
+                                                             const nwap_block_rows *br = nullptr)
 {
     unsigned long long bits = 0;
     if (k_first >= count || k_first + NWAP_CMP_PER_THREAD <= 0) {
@@ -269,7 +295,32 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
     }
     if (cand == 0) return 0;
     const int64_t kb = max(k_first, (int64_t)0);
-    int64_t r = nwap_row_of(kp.start + kb, kp.n);
+    const int64_t ke = min(k_first + (int64_t)NWAP_CMP_PER_THREAD, count) - 1;       // last live edge of this thread
+    int64_t r = -1;
+    if (br && br->r0 >= 0) {
+        if (ke < br->next1) r = br->r0;
+        else if (kb >= br->next1 && ke < br->next2) r = br->r0 + 1;
+    }
+    if (r >= 0) {
+        // all live edges of this thread lie in row r: its own length tightens the candidate bounds (m >= len_r),
+        // and the few survivors fetch their column length one byte each
+        const int lr1 = (int)kp.lens[r];
+        const short2 rb = rbounds[lr1];
+        const int64_t c0 = r + 1 + (kp.start + k_first - nwap_before_row(r, kp.n));  // column of window byte 0 (may precede the row for masked bytes)
+        unsigned long long rest = cand;
+        while (rest) {
+            const int e = __ffsll((long long)rest) - 1;
+            rest &= rest - 1;
+            const uint4 q = vec[e >> 4];
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+            const int sc = (int)(int8_t)((w4[(e >> 2) & 3] >> (8 * (e & 3))) & 0xffu);
+            if (sc < (int)rb.x || sc > (int)rb.y) continue;
+            const short2 b = bounds[max(lr1, (int)kp.lens[c0 + e])];
+            if (sc >= (int)b.x && sc <= (int)b.y) bits |= 1ull << e;
+        }
+        return bits;
+    }
+    r = nwap_row_of(kp.start + kb, kp.n);
     int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
     int lr = (int)kp.lens[r];
     if (valid == ~0ull && c + NWAP_CMP_PER_THREAD <= kp.n) {
@@ -321,13 +372,16 @@ __global__ void __launch_bounds__(NWAP_CMP_THREADS)
 k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, long long *block_counts,
                 unsigned long long *group_totals)
 {
-    __shared__ short2 bounds[MODE == 1 ? 256 : 1];
+    __shared__ short2 bounds[MODE == 1 ? 256 : 1], rbounds[MODE == 1 ? 256 : 1];
+    __shared__ nwap_block_rows brows;
     if (MODE == 1) {
         bounds[threadIdx.x] = make_short2(kp.smin[threadIdx.x], kp.smax[threadIdx.x]);     // NWAP_CMP_THREADS == 256
+        rbounds[threadIdx.x] = make_short2(kp.rmin[threadIdx.x], kp.rmax[threadIdx.x]);
+        nwap_block_rows_init(&brows, kp, nwap_cmp_first(payload) - (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD, count);
         __syncthreads();
     }
     uint4 vec[NWAP_CMP_VEC];
-    int kept = __popcll(nwap_keep_bits<MODE>(payload, count, nwap_cmp_first(payload), kp, vec, bounds));
+    int kept = __popcll(nwap_keep_bits<MODE>(payload, count, nwap_cmp_first(payload), kp, vec, bounds, rbounds, &brows));
     __shared__ int wsum[NWAP_CMP_THREADS / 32];
     kept = __reduce_add_sync(0xffffffffu, kept);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = kept;
@@ -414,14 +468,17 @@ k_compact_write(const int8_t *__restrict__ payload, int64_t count, const nwap_ke
     const long long off0 = block_offsets[blockIdx.x];
     const long long off1 = (int64_t)blockIdx.x + 1 < nblocks ? block_offsets[blockIdx.x + 1] : *total;
     if (off1 == off0) return;
-    __shared__ short2 bounds[MODE == 1 ? 256 : 1];
+    __shared__ short2 bounds[MODE == 1 ? 256 : 1], rbounds[MODE == 1 ? 256 : 1];
+    __shared__ nwap_block_rows brows;
+    const int64_t k_first = nwap_cmp_first(payload);
     if (MODE == 1) {
         bounds[threadIdx.x] = make_short2(kp.smin[threadIdx.x], kp.smax[threadIdx.x]);
+        rbounds[threadIdx.x] = make_short2(kp.rmin[threadIdx.x], kp.rmax[threadIdx.x]);
+        nwap_block_rows_init(&brows, kp, k_first - (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD, count);
         __syncthreads();
     }
-    const int64_t k_first = nwap_cmp_first(payload);
     uint4 vec[NWAP_CMP_VEC];
-    const unsigned long long bits = nwap_keep_bits<MODE>(payload, count, k_first, kp, vec, bounds);
+    const unsigned long long bits = nwap_keep_bits<MODE>(payload, count, k_first, kp, vec, bounds, rbounds, &brows);
     const int kept = __popcll(bits);
     // exclusive scan of `kept` over the block
     __shared__ int wtot[NWAP_CMP_THREADS / 32];
@@ -637,6 +694,94 @@ k_hist_normalized(const int8_t *__restrict__ payload, int64_t count, const nwap_
     __syncthreads();
     for (int b = threadIdx.x; b < NWAP_NHIST_SPAN; b += blockDim.x)
         if (sbins[b]) atomicAdd(&counts[b], (unsigned long long)sbins[b]);
+}
+
+// The same histogram without per-edge arithmetic: count the JOINT key (m, score), m = max(len_r, len_c), in
+// (mmax + 1) x 256 shared-memory bins -- per edge one byte-permute and one shared atomic, the per-4-edges maximum
+// of the lengths as byte-parallel integer ops -- and map each occupied (m, score) bin to floor(100*score / m) ONCE
+// per CTA at the end, in exact integer arithmetic (store.py:357-361).  Needs mmax <= 127 (byte-parallel max on
+// 7-bit lengths) and (mmax + 1) KB of shared memory; longer words use k_hist_normalized.
+__device__ __forceinline__ uint32_t nwap_bytemax7(uint32_t a, uint32_t b)        // per-byte max, all bytes < 128
+{
+    const uint32_t ge = (((a | 0x80808080u) - b) >> 7) & 0x01010101u;             // 1 where a >= b
+    const uint32_t mask = ge * 0xffu;
+    return (a & mask) | (b & ~mask);
+}
+
+// prmt.b32, default mode: selector nibble k < 8 copies byte k of {a, b}; nibble 8|k replicates the msb of byte k
+__device__ __forceinline__ uint32_t nwap_prmt(uint32_t a, uint32_t b, uint32_t sel)
+{
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+__global__ void __launch_bounds__(512)
+k_hist_norm_joint(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, unsigned long long *counts,
+                  int mmax)
+{
+    extern __shared__ unsigned int jbins[];              // [(mmax + 1) * 256], key = m << 8 | (score + 128)
+    const int nb = (mmax + 1) * 256;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) jbins[b] = 0;
+    __syncthreads();
+    const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload) & 15u);
+    const int64_t runs = (lead + count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
+    for (int64_t run = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; run < runs; run += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k_first = run * NWAP_CMP_PER_THREAD - lead;
+        const int64_t kb = max(k_first, (int64_t)0);
+        if (kb >= count) continue;
+        int64_t r = nwap_row_of(kp.start + kb, kp.n);
+        int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
+        int lr = (int)kp.lens[r];
+        if (k_first >= 0 && k_first + NWAP_CMP_PER_THREAD <= count && c + NWAP_CMP_PER_THREAD <= kp.n) {
+            uint32_t L[16];
+            nwap_load_lens64(kp.lens, c, L);
+            const uint32_t lr4 = (uint32_t)lr * 0x01010101u;
+#pragma unroll
+            for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+                const uint4 q4 = *reinterpret_cast<const uint4 *>(payload + k_first + 16 * v);
+                const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t x = w[q] ^ 0x80808080u;                       // score + 128 per byte
+                    const uint32_t m4 = nwap_bytemax7(L[4 * v + q], lr4);
+                    // key j = {x byte j, m4 byte j, 0, 0}: selector nibbles 8|k replicate the (clear) sign of a length byte
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xcc40u)], 1u);
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xdd51u)], 1u);
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xee62u)], 1u);
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xff73u)], 1u);
+                }
+            }
+            continue;
+        }
+#pragma unroll
+        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+            const int64_t k0 = k_first + 16 * v;
+            if (k0 + 16 <= 0 || k0 >= count) continue;
+            const uint4 q4 = nwap_cmp_load(payload, count, k0);
+            const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int64_t k = k0 + j;
+                if (k >= 0 && k < count) {
+                    const int m = max(lr, (int)kp.lens[c]);
+                    const uint32_t sb = ((w[j >> 2] >> (8 * (j & 3))) & 0xffu) ^ 0x80u;
+                    atomicAdd(&jbins[(m << 8) | (int)sb], 1u);
+                    if (++c == kp.n) { ++r; c = r + 1; lr = (int)kp.lens[min(r, kp.n - 1)]; }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int b = 256 + threadIdx.x; b < nb; b += blockDim.x) {          // m = 0 never occurs (every word has >= 1 symbol)
+        const unsigned int h = jbins[b];
+        if (h) {
+            const int m = b >> 8, num = 100 * ((b & 255) - 128);
+            int qv = num / m;
+            if (num % m != 0 && num < 0) --qv;                          // floor division
+            atomicAdd(&counts[qv - NWAP_NHIST_OFFSET], (unsigned long long)h);
+        }
+    }
 }
 
 __global__ void k_rows_cols(int64_t n, const int64_t *idx, int64_t count, int64_t *rows, int64_t *cols)

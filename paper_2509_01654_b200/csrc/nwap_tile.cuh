@@ -63,10 +63,13 @@ struct nwap_keep_params {
     // two integer compares and exactly the reference's keep-mask; an empty interval is smin > smax.
     int8_t smin[256], smax[256];
     int gmin, gmax;          // MODE 1: loosest bounds over all lengths (gmin > gmax: nothing can be kept)
+    // MODE 1: loosest bounds over the lengths m >= l (up to the longest word): what a score in a row whose word has
+    // l symbols must satisfy whatever the column is, since m = max(len_r, len_c) >= len_r.  Empty: rmin > rmax.
+    int8_t rmin[256], rmax[256];
 };
 
 // host side of the table above
-inline void nwap_fill_norm_bounds(nwap_keep_params &kp, double lo, double hi)
+inline void nwap_fill_norm_bounds(nwap_keep_params &kp, double lo, double hi, int qmax = 255)
 {
     for (int m = 0; m < 256; ++m) {
         int first = 1, last = 0;                     // empty
@@ -81,6 +84,15 @@ inline void nwap_fill_norm_bounds(nwap_keep_params &kp, double lo, double hi)
     kp.gmin = 127; kp.gmax = -128;
     for (int m = 1; m < 256; ++m)
         if (kp.smin[m] <= kp.smax[m]) { kp.gmin = kp.gmin < kp.smin[m] ? kp.gmin : kp.smin[m]; kp.gmax = kp.gmax > kp.smax[m] ? kp.gmax : kp.smax[m]; }
+    int lo_s = 127, hi_s = -128;                      // running loosest bounds over m in [l, qmax]
+    for (int l = 255; l >= 0; --l) {
+        if (l >= 1 && l <= qmax && kp.smin[l] <= kp.smax[l]) {
+            lo_s = lo_s < kp.smin[l] ? lo_s : kp.smin[l];
+            hi_s = hi_s > kp.smax[l] ? hi_s : kp.smax[l];
+        }
+        kp.rmin[l] = (int8_t)(lo_s <= hi_s ? lo_s : 1);
+        kp.rmax[l] = (int8_t)(lo_s <= hi_s ? hi_s : 0);
+    }
 }
 
 // MODE 0: bit j of the result = (signed byte j of the 4 words >= threshold), 4 bytes per SWAR step.
@@ -123,7 +135,7 @@ struct nwap_tile_params {
     int64_t unit_count;
     unsigned long long *unit_counter;
     nwap_dev_stats *stats;
-    int want_hist;
+    int want_hist;                 // unused by the tile kernel (see k_payload_stats); kept for the generic kernel's twin struct
     const nwap_ov_row *ov_table;   // sparse-override mode: (ov_K) rows on the device, else NULL
     int ov_K;                      // alphabet size K of the override / dense table
     const uint8_t *etab;           // dense-table mode (FLAVOR 3): K x K table of M - sim on the device, else NULL
@@ -161,7 +173,6 @@ struct nwap_tile_smem_t {
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
     uint8_t clen[NWAP_C];         // their lengths
     int bins[NWAP_WARPS][MAXLEN + 2];
-    unsigned int hist[256];
     short2 kbounds[256];          // sparse-output mode, normalised filter: per-length score bounds
     unsigned long long unit;
     long long sum;
@@ -236,14 +247,12 @@ __device__ __forceinline__ void nwap_emit(SM &sm, const nwap_row_meta &m, uint32
             ls.sum += s0; ls.count += 1;
             ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffff0000u) | (t & 0xffffu));
             ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffff0000u) | (t & 0xffffu));
-            if (want_hist) atomicAdd(&sm.hist[(s0 + 128) & 255], 1u);
         }
         if (c.off1 - clo < seg) {
             sm.out[adj + (int)c.off1] = (uint8_t)(int8_t)s1;
             ls.sum += s1; ls.count += 1;
             ls.mn2 = __vmins2(ls.mn2, (ls.mn2 & 0xffffu) | (t & 0xffff0000u));
             ls.mx2 = __vmaxs2(ls.mx2, (ls.mx2 & 0xffffu) | (t & 0xffff0000u));
-            if (want_hist) atomicAdd(&sm.hist[(s1 + 128) & 255], 1u);
         }
     }
 }
@@ -496,10 +505,18 @@ __device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_
 
 // One chunk whose longest word exceeds the register-resident row: block-wise DP (nwap_dp_blocks), per-lane
 // selection of the final cell, shared epilogue.  Rare by construction (words of 25..64 symbols in a wide
-// build), kept out of line so its registers and its 260-byte per-lane boundary column do not weigh on the
-// length-specialised bodies.
+// build).  Inlined: out of line (generic addressing of the shared row symbols, call ABI) the wide build lost
+// 3.1 % on a vocabulary with no long word at all, inlined 1.4 % (gpurun A/B, 100,000 words).
+#ifndef NWAP_WIDE_INLINE
+#define NWAP_WIDE_INLINE 1
+#endif
+#if NWAP_WIDE_INLINE
+#define NWAP_WIDE_ATTR __forceinline__
+#else
+#define NWAP_WIDE_ATTR __noinline__
+#endif
 template <class SM>
-__device__ __noinline__ void nwap_run_chunk_wide(int LB, SM &sm, const nwap_scheme_consts &sc, const uint8_t *b0,
+__device__ NWAP_WIDE_ATTR void nwap_run_chunk_wide(int LB, SM &sm, const nwap_scheme_consts &sc, const uint8_t *b0,
                                                  const uint8_t *b1, const nwap_lane_cols &c, bool fast, int want_hist,
                                                  nwap_lane_stats &ls)
 {
@@ -626,7 +643,9 @@ k_score_tiles(const nwap_tile_params p)
     static_assert(!WIDE || (FLAVOR == 1 && !OV && QMAX == 24), "the wide build exists for the default uniform-scheme cell only");
 
     if (tid == 0) { sm.sum = 0; sm.count = 0; sm.mn = 127; sm.mx = -128; }
-    for (int b = tid; b < 256; b += NWAP_THREADS) sm.hist[b] = 0;
+    // the 256-bin histogram is not accumulated here: a request for it is served by k_payload_stats over the
+    // scored bytes (5.5 TB/s), so every chunk keeps the fast emit (per-edge shared atomics cost far more)
+    constexpr int kNoHist = 0;
     if (FLAVOR == 3) {
         for (int w = tid; w < p.ov_K * p.ov_K; w += NWAP_THREADS) sm.etab[w] = p.etab[w];
     }
@@ -753,7 +772,7 @@ k_score_tiles(const nwap_tile_params p)
             // every thread from launch scalars: no extra barrier, nothing read back from shared memory.
             const bool clip_first = p.r_first >= rb0 && p.r_first < rb0 + NWAP_R && p.c_start > strip_lo;
             const bool clip_last = p.r_last >= rb0 && p.r_last < rb0 + NWAP_R && p.c_end + 1 < strip_hi;
-            const bool band_simple = !p.want_hist && rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax &&
+            const bool band_simple = rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax &&
                                      rb0 + NWAP_R - 1 < strip_lo && !clip_first && !clip_last;
 
             // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
@@ -788,21 +807,21 @@ k_score_tiles(const nwap_tile_params p)
                 const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
                 const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
                 if (WIDE && LB > QMAX) {
-                    nwap_run_chunk_wide(LB, sm, sc, p.ids + ca * p.qpad, p.ids + cb * p.qpad, cA, fast, p.want_hist, ls);
+                    nwap_run_chunk_wide(LB, sm, sc, p.ids + ca * p.qpad, p.ids + cb * p.qpad, cA, fast, kNoHist, ls);
                     continue;
                 }
                 if (FLAVOR == 3) {
-                    nwap_run_chunk_tab<QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+                    nwap_run_chunk_tab<QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
                     continue;
                 }
 #if NWAP_HOIST
                 // two code families only where the register budget allows (the 32-wide and sparse-override
                 // instantiations would spill): there the hoisted bodies also carry the slow emit
                 constexpr bool FASTONLY = NWAP_HOIST_FASTONLY && QMAX <= 24 && !OV;
-                if (!FASTONLY || fast) nwap_run_chunk_h<FLAVOR, QMAX, QW, FASTONLY>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
-                else nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+                if (!FASTONLY || fast) nwap_run_chunk_h<FLAVOR, QMAX, QW, FASTONLY>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
+                else nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
 #else
-                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, p.want_hist, ls);
+                nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
 #endif
             }
             __syncthreads();
@@ -859,9 +878,6 @@ k_score_tiles(const nwap_tile_params p)
         atomicMin(&p.stats->mn, sm.mn);
         atomicMax(&p.stats->mx, sm.mx);
     }
-    if (p.want_hist)
-        for (int b = tid; b < 256; b += NWAP_THREADS)
-            if (sm.hist[b]) atomicAdd(&p.stats->hist[b], (unsigned long long)sm.hist[b]);
 }
 
 

@@ -361,9 +361,16 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
                       devices: Optional[Sequence[int]] = None) -> ComputeStats:
     """Drop-in for reference engine.py:218-290.
 
-    Every edge score goes through ``sink.write`` once, in linear-index order, in
-    pieces of ``plan.chunk_size`` edges (the payload never depends on it); on any
-    failure ``sink.abort()`` is called before the exception propagates.
+    Every edge score goes through the sink once, in linear-index order, in pieces of
+    ``plan.chunk_size`` edges (the payload never depends on it); on any failure after the
+    arguments have been validated ``sink.abort()`` is called before the exception propagates.
+
+    Sink protocol.  ``sink.write(data)`` receives an immutable ``bytes`` object per piece, exactly as
+    the reference passes (engine.py:256, :272), so sinks that keep the object (the reference tests'
+    ``chunks.append(data)``) stay correct.  A sink that consumes the data before returning can opt into
+    the zero-copy path by defining ``write_view(view)``: it is then called instead, with a memoryview
+    into a pinned staging slab that is ONLY VALID DURING THE CALL (the slab is overwritten two slabs
+    later and recycled by the next run).  ``PipelinedEdgeStoreWriter`` does.
 
     ``devices`` (default ``[device]``) lists the GPUs to use from this one process -- the
     counterpart of the reference's fork pool (engine.py:262-276): slab k of the edge range
@@ -371,6 +378,9 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
     consumes the slabs in index order, so the payload is the same for any G
     (partition invariance, tests/test_engine.py:92-101).  The word store is replicated; no
     edge byte moves between GPUs.
+
+    Deviation from the reference: phoneme ids must fit one byte (alphabet <= 256 symbols; the
+    reference packs int32).  Larger ids raise DataError.
     """
     import torch
 
@@ -385,10 +395,7 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
     devs = [int(d) for d in (devices if devices is not None else [device])]
     if not devs:
         raise ValueError("devices must name at least one GPU")
-    if not torch.cuda.is_available():
-        raise RuntimeError("compute_all_pairs needs a CUDA device: there is no CPU fallback")
 
-    ids, lengths = pack_words(words, q)
     total = num_edges(n)
     edges = 0
     score_sum = 0
@@ -397,12 +404,16 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
     started = time.perf_counter()
     ctxs: list = []
     staging: list = []
+    emit_view = getattr(sink, "write_view", None)
     try:
+        if not torch.cuda.is_available():
+            raise RuntimeError("compute_all_pairs needs a CUDA device: there is no CPU fallback")
+        ids, lengths = pack_words(words, q)
         chunk = plan.chunk_size
         # pinned host slabs of a whole number of sink chunks (about 64 MiB each), two per GPU: the devices
         # score and copy the next slabs while the sink consumes slab k, in index order
         slab = max(chunk, (_SLAB_BYTES // chunk) * chunk)
-        slab = min(slab, -(-total // chunk) * chunk)
+        slab = min(slab, total)              # a chunk_size beyond the job is one piece (and pins no more than the job)
         ranges = [(s, min(s + slab, total)) for s in range(0, total, slab)]
         G = max(1, min(len(devs), len(ranges)))
         ctxs = [NwapContext(ids, lengths, scheme, d) for d in devs[:G]]
@@ -427,7 +438,10 @@ def compute_all_pairs(words: Sequence, scheme, sink, plan: Optional[ComputePlan]
             view = views[buf(k)]
             for cs in range(0, e - s, chunk):
                 piece = view[cs: min(cs + chunk, e - s)]
-                sink.write(piece)
+                if emit_view is not None:
+                    emit_view(piece)          # transient: valid during the call only
+                else:
+                    sink.write(bytes(piece))  # what the reference hands over: an immutable bytes object
                 edges += len(piece)
             score_sum += ssum
             score_min = min(score_min, smin)
@@ -465,9 +479,21 @@ def _staging_slabs(nbytes: int, count: int):
     return out
 
 
+_STAGING_CACHE_BYTES = 512 << 20      # pinned bytes kept between runs (two slabs per GPU for 4 GPUs)
+
+
 def _return_slabs(slabs) -> None:
     with _STAGING_LOCK:
+        held = sum(t.numel() for have in _STAGING.values() for t in have)
         for t in slabs:
-            have = _STAGING.setdefault(t.numel(), [])
-            if len(have) < 16:
-                have.append(t)
+            if held + t.numel() <= _STAGING_CACHE_BYTES:
+                _STAGING.setdefault(t.numel(), []).append(t)
+                held += t.numel()
+
+
+def trim() -> None:
+    """Release everything cached between runs: the pinned staging slabs here and the per-device pipelines
+    and memory-pool blocks inside the library (nwap_trim)."""
+    with _STAGING_LOCK:
+        _STAGING.clear()
+    lib().nwap_trim()

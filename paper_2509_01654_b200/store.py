@@ -206,6 +206,10 @@ class PipelinedEdgeStoreWriter:
             raise DataError(f"payload overflow: {self._written} bytes written, "
                             f"expected {self.expected_bytes}")
 
+    # write() copies the data into the writer's own blocks before it returns, so it may be handed transient views
+    # (engine.compute_all_pairs calls write_view, when a sink has one, with a view into a recycled pinned slab)
+    write_view = write
+
     def _drain(self) -> None:
         self._flush_block()
         for st in (self._hasher, self._filer):
@@ -295,3 +299,80 @@ def words_to_store(words: Sequence) -> Tuple[np.ndarray, np.ndarray]:
     """The uint8 word store (ids (n, q), lengths (n,)) of a word list: engine.pack_words."""
     from .engine import pack_words
     return pack_words(words)
+
+
+# ---------------------------------------------------------------------------------------------
+# inventory sidecar (corpus.py:91-118) and scheme files (aligner.py:195-239): what `compute --scheme FILE` reads
+# ---------------------------------------------------------------------------------------------
+
+def load_inventory(path) -> dict:
+    """``token<TAB>id`` per line, ids dense 0..K-1 (corpus.py:97-118).  Returns {token: id}."""
+    by_id = {}
+    with open(path, encoding="utf-8") as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            line = raw.rstrip("\n")
+            if not line:
+                continue
+            fields = line.split("\t")
+            if len(fields) != 2:
+                raise DataError(f"{path}: line {lineno}: expected 'token<TAB>id'")
+            try:
+                ident = int(fields[1])
+            except ValueError:
+                raise DataError(f"{path}: line {lineno}: bad id {fields[1]!r}") from None
+            if ident in by_id:
+                raise DataError(f"{path}: line {lineno}: duplicate id {ident}")
+            by_id[ident] = fields[0]
+    if not by_id:
+        raise DataError(f"{path}: inventory file is empty")
+    if sorted(by_id) != list(range(len(by_id))):
+        raise DataError(f"{path}: ids are not dense 0..{len(by_id) - 1}")
+    id_of = {tok: i for i, tok in by_id.items()}
+    if len(id_of) != len(by_id):
+        raise DataError("inventory contains duplicate phoneme tokens")
+    return id_of
+
+
+def load_scheme_file(path, id_of=None):
+    """A scheme file (aligner.py:195-239): tab-separated ``match|mismatch|gap <TAB> int`` declarations (all three
+    required) and ``tokenA <TAB> tokenB <TAB> int`` symmetric per-pair overrides, which need an inventory
+    (``id_of``: {token: id}) to resolve; blank lines and ``#`` comments are skipped.  Same ``DataError``
+    messages as the reference."""
+    from .host_types import ScoringScheme
+
+    core, overrides = {}, {}
+    with open(path, encoding="utf-8") as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            line = raw.strip()
+            if not line or line[0] == "#":
+                continue
+            fields = line.split("\t")
+            where = f"{path}: line {lineno}"
+            if len(fields) == 2:
+                key, text = fields
+                if key not in ("match", "mismatch", "gap"):
+                    raise DataError(f"{where}: unknown key {key!r}")
+                try:
+                    core[key] = int(text)
+                except ValueError:
+                    raise DataError(f"{where}: {key} must be an integer") from None
+            elif len(fields) == 3:
+                if id_of is None:
+                    raise DataError(f"{where}: per-pair overrides require an inventory")
+                try:
+                    value = int(fields[2])
+                except ValueError:
+                    raise DataError(f"{where}: override must be an integer") from None
+                for tok in fields[:2]:
+                    if tok not in id_of:
+                        raise DataError(f"{where}: unknown phoneme {tok!r}")
+                a, b = id_of[fields[0]], id_of[fields[1]]
+                overrides[(a, b)] = value
+                overrides[(b, a)] = value
+            else:
+                raise DataError(f"{where}: expected 2 or 3 tab-separated fields")
+    for key in ("match", "mismatch", "gap"):
+        if key not in core:
+            raise DataError(f"{path}: missing required key {key!r}")
+    return ScoringScheme(core["match"], core["mismatch"], core["gap"], overrides)
+

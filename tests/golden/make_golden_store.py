@@ -55,6 +55,13 @@ def main():
                     "--workers", "1", "--chunk-size", "37", "--out", str(OUT / f"toy_{tag}")])
         text = re.sub(r"in \d+\.\d+ s", "in <T> s", text).replace(str(OUT) + "/", "")
         printed[tag] = {"scheme": [m, x, g], "stdout": text}
+    # a scheme FILE with per-pair overrides (cli.py:167-174, aligner.py:195-239), resolved against toy.inventory
+    (OUT / "scheme_s3.txt").write_text("# nasal vowels and the two affricates count as near-matches\nmatch\t2\nmismatch\t-1\n"
+                                       "gap\t-2\n\n\u0251\u0303\t\u025b\u0303\t1\nt\u0283\td\u0292\t1\n\u0283\ts\t0\n", encoding="utf-8")
+    text = run(["compute", str(OUT / "toy.words"), "--scheme", str(OUT / "scheme_s3.txt"), "--workers", "2",
+                "--chunk-size", "50", "--out", str(OUT / "toy_s3")])
+    text = re.sub(r"in \d+\.\d+ s", "in <T> s", text).replace(str(OUT) + "/", "")
+    printed["s3"] = {"scheme_file": "scheme_s3.txt", "stdout": text}
     (OUT / "compute_stdout.json").write_text(json.dumps(printed, ensure_ascii=False, indent=1), encoding="utf-8")
     for p in sorted(OUT.iterdir()):
         print(p.name, p.stat().st_size)

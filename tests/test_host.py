@@ -63,7 +63,7 @@ def test_no_cpu_fallback():
     sink = CollectSink()
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         nw.compute_all_pairs(synth.make_words(5, seed=0), nw.ScoringScheme(), sink)
-    assert not sink.chunks
+    assert not sink.chunks and sink.aborted      # the sink is told, so a writer can mark its store incomplete
 
 
 def test_scheme_semantics():
