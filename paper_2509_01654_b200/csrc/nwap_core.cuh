@@ -41,7 +41,9 @@
 #include <stdint.h>
 #include "nwap_index.cuh"
 
+#ifndef NWAP_BIAS
 #define NWAP_BIAS 8192u
+#endif
 #define NWAP_BIAS2 (NWAP_BIAS | (NWAP_BIAS << 16))
 
 struct nwap_scheme_consts {
@@ -51,7 +53,8 @@ struct nwap_scheme_consts {
     uint32_t one;         // 1, opaque to the compiler so `cur*one+u2` stays an IMAD
     int32_t alpha;        // row potential per symbol:    match - gap (FLAVOR 0/1), gap (FLAVOR 2)
     int32_t beta;         // column potential per symbol: gap
-    uint32_t symmul;      // staged row symbol = a * symmul:  65537 (FLAVOR 0/1), 256*65537 (FLAVOR 2)
+    uint32_t symmul;      // staged row symbol = a * symmul + symadd:  65537, 0 (FLAVOR 0); -65537, 0x01000100 (FLAVOR 1:
+    uint32_t symadd;      // halves 256 - a, see nwap_pack_negb_f); 256*65537, 0 (FLAVOR 2); K, 0 (FLAVOR 3: table row offset)
     uint32_t t2;          // FLAVOR 2: D * 65537, the add-min threshold
     uint32_t c2;          // FLAVOR 2: (match - 2*gap) * 65537
 };
@@ -70,6 +73,8 @@ NWAP_HD nwap_scheme_consts nwap_make_consts(int match, int mismatch, int gap, in
     c.alpha = match - gap;
     c.beta = gap;
     c.symmul = 65537u;
+    c.symadd = 0u;
+    if (flavor == 1) { c.symmul = 0u - 65537u; c.symadd = 0x01000100u; }
     c.t2 = 0u;
     c.c2 = 0u;
     if (flavor == 3) {
@@ -87,6 +92,8 @@ NWAP_HD nwap_scheme_consts nwap_make_consts(int match, int mismatch, int gap, in
     }
     return c;
 }
+
+NWAP_HD uint32_t nwap_row_code(uint32_t a, const nwap_scheme_consts &sc) { return a * sc.symmul + sc.symadd; }
 
 // ---- DPX intrinsics with host emulation ------------------------------------
 #if defined(__CUDA_ARCH__)
@@ -149,10 +156,17 @@ NWAP_HD uint32_t nwap_pack_negb(uint32_t b0, uint32_t b1)
     return ((0u - b0) & 0xffffu) | ((0u - b1) << 16);
 }
 // FLAVOR 2 stores symbols times 256 (see the header comment).
+// FLAVOR 1 (the default cell) moves the minus sign to the row side so that the column side is a pure byte
+// interleave: the column code of symbol b is b + 0xff00 = (b - 256) mod 2^16 -- bytes {b0, 0xff, b1, 0xff}, two byte
+// permutes per two columns (nwap_unpack_cols) instead of five shift/mask/negate operations per column -- and the
+// staged row code is 256 - a in both halves (a * -65537 + 0x01000100: no borrow, 256 - a >= 1), so that
+// (row + column) mod 2^16 = b - a is still zero exactly where the symbols are equal.
 template <int FLAVOR>
 NWAP_HD uint32_t nwap_pack_negb_f(uint32_t b0, uint32_t b1)
 {
-    return FLAVOR == 2 ? nwap_pack_negb(b0 << 8, b1 << 8) : nwap_pack_negb(b0, b1);
+    return FLAVOR == 2 ? nwap_pack_negb(b0 << 8, b1 << 8)
+         : FLAVOR == 1 ? ((b0 | 0xff00u) | ((b1 | 0xff00u) << 16))
+                       : nwap_pack_negb(b0, b1);
 }
 
 // One score-matrix row (one symbol of the row word, packed as a*65537) against
@@ -210,32 +224,28 @@ struct nwap_sym2 { uint32_t a2, left0; };
 #ifndef NWAP_PREFETCH
 #define NWAP_PREFETCH 0
 #endif
-//   NWAP_PEEL 1: the first matrix row is peeled (H'[0][j] = BIAS is folded in: no row initialisation,
-//                no up+u add in that row), the loop runs the remaining la-1 rows
-#ifndef NWAP_PEEL
-#define NWAP_PEEL 0
-#endif
 //   NWAP_DUFF_MAXLB n: length bodies up to n run two matrix rows per loop trip (0 = off)
 #ifndef NWAP_DUFF_MAXLB
 #define NWAP_DUFF_MAXLB 0
 #endif
 
-template <int LB, int FLAVOR>
+// PEEL (FLAVOR 1 only): matrix row 1 is peeled.  Every H'[0][j] is BIAS, so its diagonal term is BIAS - e*D, and
+// its up term BIAS + u equals the row's boundary value H'[1][0] the left chain starts from, i.e. it is absorbed:
+// H'[1][j] = max(BIAS - e_j*D, H'[1][j-1]) -- three instructions per cell instead of four and no initialisation of
+// the rolling row.  Costs 3*LB + 4 instructions of code per body, so only short bodies use it (NWAP_F2_PEEL_MAXLB).
+template <int LB, int FLAVOR, bool PEEL = false>
 NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
                           uint32_t (&P)[LB + 1], const nwap_scheme_consts &sc)
 {
-#if NWAP_PEEL
-    if (FLAVOR == 1) {
-        // matrix row 1: every H'[0][j] is BIAS, so diag and up+u are constants and nothing is read from P
+    if (PEEL && FLAVOR == 1) {
         const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
         const nwap_sym2 x0 = *s++;
-        const uint32_t bu = NWAP_BIAS2 + sc.u2;
         uint32_t left = x0.left0;
         P[0] = NWAP_BIAS2;
 #pragma unroll
         for (int j = 1; j <= LB; ++j) {
             const uint32_t dw = nwap_viaddmin_u16x2(x0.a2, nb[j - 1], 0x00010001u) * sc.neg_delta + NWAP_BIAS2;
-            left = nwap_vimax3_s16x2(dw, bu, left);
+            left = nwap_vmaxs2(dw, left);
             P[j] = left;
         }
         uint32_t d0 = x0.left0;
@@ -247,7 +257,6 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
         }
         return;
     }
-#endif
 #pragma unroll
     for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;        // H'[0][j]
     uint32_t d0 = NWAP_BIAS2;                               // H'[0][0]
@@ -324,7 +333,7 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
 // Rows whose symbol has no partner run the plain cell.
 #define NWAP_MAX_OV 3
 struct nwap_ov_row {                 // one row of the per-symbol override table
-    uint32_t b2[NWAP_MAX_OV];        // partner symbol * 65537 (unused slot: anything)
+    uint32_t b2[NWAP_MAX_OV];        // partner symbol as a row code (FLAVOR 1: 256 - b in both halves; unused slot: anything)
     uint32_t nd[NWAP_MAX_OV];        // (uint32)(-delta_k)     (unused slot: 0)
     uint32_t dsum;                   // (uint32)(sum_k delta_k) * 65537 ... packed for both halves
     uint32_t count;                  // number of used slots
@@ -383,7 +392,7 @@ inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatc
             const int delta = (int)sim[a * K + b] - (a == b ? match : mismatch);
             if (delta == 0) continue;
             if (cnt == NWAP_MAX_OV) return false;
-            r.b2[cnt] = (uint32_t)b * 65537u;
+            r.b2[cnt] = 0x01000100u - (uint32_t)b * 65537u;
             r.nd[cnt] = (uint32_t)(-delta);
             dsum += delta;
             ++cnt;
@@ -456,9 +465,9 @@ NWAP_HD void nwap_load_block_negb(const uint8_t *b0, const uint8_t *b1, uint32_t
     const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, yw[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
     for (int j = 0; j < NWAP_WB; ++j)
-        nb[j] = nwap_pack_negb((xw[j >> 2] >> (8 * (j & 3))) & 0xffu, (yw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+        nb[j] = nwap_pack_negb_f<1>((xw[j >> 2] >> (8 * (j & 3))) & 0xffu, (yw[j >> 2] >> (8 * (j & 3))) & 0xffu);
 #else
-    for (int j = 0; j < NWAP_WB; ++j) nb[j] = nwap_pack_negb(b0[j], b1[j]);
+    for (int j = 0; j < NWAP_WB; ++j) nb[j] = nwap_pack_negb_f<1>(b0[j], b1[j]);
 #endif
 }
 
@@ -494,12 +503,12 @@ NWAP_HD uint32_t nwap_dp_blocks(const nwap_sym2 *row_sym2, int la, const uint8_t
 // Whole pair-of-pairs DP for one row word; returns the packed H' values at
 // (la, lb0) in the low half and (la, lb1) in the high half.  Used by the host
 // emulation test; the tile kernel calls nwap_dp_word directly.
-template <int LB, int FLAVOR>
+template <int LB, int FLAVOR, bool PEEL = false>
 NWAP_HD uint32_t nwap_dp_pair(const nwap_sym2 *row_sym2, int la, const uint32_t (&nb)[LB],
                               int lb0, int lb1, const nwap_scheme_consts &sc)
 {
     uint32_t P[LB + 1];
-    nwap_dp_word<LB, FLAVOR>(row_sym2, la, nb, P, sc);
+    nwap_dp_word<LB, FLAVOR, PEEL>(row_sym2, la, nb, P, sc);
     uint32_t lo = 0, hi = 0;
 #pragma unroll
     for (int j = 1; j <= LB; ++j) {

@@ -143,15 +143,17 @@ struct nwap_tile_params {
 };
 
 struct alignas(16) nwap_row_meta {
-    // first 16 bytes: everything the fast row path needs, one LDS.128
+    // first 16 bytes: everything the fast row path needs
     int la;            // row word length, 0 = row not in this launch / no valid column in this strip
+    uint32_t symend;   // shared-window address one past the row's last staged symbol record (matrix-row loop bound)
     uint32_t ala2;     // (alpha * la) * 65537: the row potential, packed for both halves
     int rowadj;        // smem byte index of (column offset 0): rr*PITCH + skew - clo_off
-    int skew;          // (global address of the segment) & 15
     int clo_off;       // first valid column, relative to the strip
     int seglen;        // number of valid columns in this strip for this row
     int64_t g0;        // out-relative byte offset of the segment
 };
+// (global address of the row's segment) & 15: the staged row is skewed so shared and global addresses agree mod 16
+__device__ __forceinline__ int nwap_meta_skew(const nwap_row_meta &m, int rr) { return m.rowadj - rr * NWAP_PITCH + m.clo_off; }
 
 // ---------------------------------------------------------------------------
 // shared memory carve-up of k_score_tiles
@@ -169,7 +171,7 @@ struct nwap_tile_smem_t {
     alignas(16) sym_t rowsym[NWAP_R][MAXLEN + 1];                // {a*65537, H'[i+1][0] (, override row)} per matrix row
     alignas(16) nwap_ov_row ov[MODE == 1 ? NWAP_OV_MAXK : 1];       // per-symbol override table (sparse-override mode)
     alignas(16) uint8_t etab[MODE == 2 ? NWAP_OV_MAXK * NWAP_OV_MAXK : 16];   // dense-table mode
-    alignas(16) nwap_row_meta meta[NWAP_R];
+    alignas(16) nwap_row_meta meta[NWAP_R + 1];                     // one readable record past the band (row prefetch)
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
     uint8_t clen[NWAP_C];         // their lengths
     int bins[NWAP_WARPS][MAXLEN + 2];
@@ -187,6 +189,24 @@ typedef nwap_tile_smem_t<0> nwap_tile_smem;
 __device__ __forceinline__ uint32_t nwap_byte_of(const uint32_t *w, int j)
 {
     return (w[j >> 2] >> (8 * (j & 3))) & 0xffu;
+}
+
+// Column codes of the lane's two words for matrix columns 0..N-1 (nwap_pack_negb_f).  FLAVOR 1: byte permutes only --
+// {A0 A1 B0 B1} per two columns, then {A0 ff B0 ff} and {A1 ff B1 ff}: three PRMT per two columns.
+template <int FLAVOR, int N, int QW>
+__device__ __forceinline__ void nwap_unpack_cols(const uint32_t (&w0)[QW], const uint32_t (&w1)[QW], uint32_t (&nb)[N])
+{
+    if (FLAVOR == 1) {
+#pragma unroll
+        for (int j = 0; j < N; j += 2) {
+            const uint32_t t = __byte_perm(w0[j >> 2], w1[j >> 2], (j & 2) ? 0x7632u : 0x5410u);
+            nb[j] = __byte_perm(t, 0xffffffffu, 0x4240u);
+            if (j + 1 < N) nb[j + 1] = __byte_perm(t, 0xffffffffu, 0x4341u);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) nb[j] = nwap_pack_negb_f<FLAVOR>(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    }
 }
 
 // Statistics are kept packed: t = H' + row potential + column potential has halves
@@ -334,7 +354,7 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
 {
     uint32_t nb[QMAX];
 #pragma unroll
-    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb_f<FLAVOR>(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    nwap_unpack_cols<FLAVOR, QMAX, QW>(w0, w1, nb);
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
     const bool deep = mixmode > 2;
     const int l0 = c.l0, l1 = c.l1;
@@ -452,7 +472,7 @@ __device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_cons
             uint32_t v, vm1, vm2;
             nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, (int)cur.x, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
             if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
-            nwap_emit(sm, sm.meta[rr], cur.y, (int)cur.z, v, c, nwap_true(), 0, ls, ca);
+            nwap_emit(sm, sm.meta[rr], cur.z, (int)cur.w, v, c, nwap_true(), 0, ls, ca);
         }
         return;
     }
@@ -477,7 +497,7 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
 {
     uint32_t nb[QMAX];
 #pragma unroll
-    for (int j = 0; j < QMAX; ++j) nb[j] = nwap_pack_negb_f<FLAVOR>(nwap_byte_of(w0, j), nwap_byte_of(w1, j));
+    nwap_unpack_cols<FLAVOR, QMAX, QW>(w0, w1, nb);
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
@@ -489,17 +509,227 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
 }
 
 
+// ---- the fast family, second shape (NWAP_FAST2=1) -------------------------------------------------------------
+// Serves chunks that are full, whose rows all cover the whole column window, and whose lanes span at most three
+// word lengths (mixmode <= 2) -- everything else goes through the compact per-row-dispatch family.  Compared with
+// nwap_chunk_rows_h it executes fewer instructions per row word:
+//   * no deep select and no mixmode tests: the final cell is always merged from the last three columns;
+//   * the negated column symbols are unpacked inside the length body (LB of them, not QMAX);
+//   * the packed sum is one IDP.2A (lo + hi into a 32-bit accumulator) instead of two adds;
+//   * row metadata and row symbols are walked by pointer (meta[] has one readable record past the band);
+//   * bodies up to NWAP_F2_PEEL_MAXLB peel the first matrix row (nwap_dp_word<.., PEEL>).
+#ifndef NWAP_FAST2
+#define NWAP_FAST2 1
+#endif
+#ifndef NWAP_F2_PEEL_MAXLB
+#define NWAP_F2_PEEL_MAXLB 8
+#endif
+#ifndef NWAP_F2_DP2A
+#define NWAP_F2_DP2A 0
+#endif
+#ifndef NWAP_F2_SHARED_UNPACK
+#define NWAP_F2_SHARED_UNPACK 0
+#endif
+#ifndef NWAP_F2_LEANHEAD
+#define NWAP_F2_LEANHEAD 0
+#endif
+#ifndef NWAP_F2_KPOS_REG
+#define NWAP_F2_KPOS_REG 0
+#endif
+#ifndef NWAP_F2_MULHI
+#define NWAP_F2_MULHI 0
+#endif
+// sensitivity experiments only (never in a shipped build): drop the min/max update, add n FMA-pipe / ALU-pipe
+// instructions per row word
+#ifndef NWAP_X_NOMM
+#define NWAP_X_NOMM 0
+#endif
+#ifndef NWAP_X_FMA
+#define NWAP_X_FMA 0
+#endif
+#ifndef NWAP_X_ALU
+#define NWAP_X_ALU 0
+#endif
+// shared-window loads by 32-bit address: one induction variable serves both the load and the loop test (with
+// generic pointers ptxas keeps two copies of it, one per use)
+__device__ __forceinline__ uint2 nwap_lds64(uint32_t addr)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t nwap_lds32(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint4 nwap_lds128(uint32_t addr)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void nwap_sts8(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.shared.u8 [%0], %1;" :: "r"(addr), "r"(v));
+}
+
+template <int LB, int FLAVOR, int QW, class SM>
+__device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_consts &sc, const uint32_t (&w0)[QW],
+                                                      const uint32_t (&w1)[QW], const uint32_t *nbq,
+                                                      const nwap_lane_cols &c, nwap_lane_stats &ls)
+{
+    constexpr bool PEEL = LB <= NWAP_F2_PEEL_MAXLB && FLAVOR == 1;
+    uint32_t nb[LB];
+#if NWAP_F2_SHARED_UNPACK
+#pragma unroll
+    for (int j = 0; j < LB; ++j) nb[j] = nbq[j];
+#else
+    nwap_unpack_cols<FLAVOR, LB, QW>(w0, w1, nb);
+#endif
+    uint32_t acc = 0, acc_hi = 0;
+    const uint32_t out_s = (uint32_t)__cvta_generic_to_shared(sm.out);
+    const uint32_t o0 = out_s + c.off0, o1 = out_s + c.off1;
+    uint32_t kpos2 = c.kpos2;
+#if NWAP_F2_KPOS_REG
+    asm volatile("" : "+r"(kpos2));                              // keep it in a register (else it is rebuilt per row)
+#endif
+    uint32_t sym_s = (uint32_t)__cvta_generic_to_shared(&sm.rowsym[0][0]);
+    uint32_t meta_s = (uint32_t)__cvta_generic_to_shared(&sm.meta[0]);
+    constexpr uint32_t SYM_PITCH = sizeof(sm.rowsym[0]);
+    constexpr uint32_t META_PITCH = sizeof(nwap_row_meta);
+#if NWAP_F2_LEANHEAD
+    uint32_t ea_next = nwap_lds32(meta_s + 4u);
+#else
+    uint4 nxt = nwap_lds128(meta_s);
+#endif
+#pragma unroll 1
+    for (int rr = 0; rr < NWAP_R; ++rr) {
+#if NWAP_F2_LEANHEAD
+        // the loop bound is fetched a row ahead; {ala2, rowadj} are fetched now and used after the matrix rows
+        const uint32_t ea = ea_next;
+        const uint2 cur = nwap_lds64(meta_s + 8u);
+        ea_next = nwap_lds32(meta_s + META_PITCH + 4u);          // meta[] has one readable record past the band
+        meta_s += META_PITCH;
+#else
+        // the whole 16-byte record {la, symend, ala2, rowadj} is fetched a row ahead
+        const uint32_t ea = nxt.y;
+        const uint2 cur = make_uint2(nxt.z, nxt.w);
+        meta_s += META_PITCH;
+        nxt = nwap_lds128(meta_s);                               // meta[] has one readable record past the band
+#endif
+        uint32_t P[LB + 1];
+        uint32_t sa = sym_s;
+        sym_s += SYM_PITCH;
+        uint32_t d0;
+        if (PEEL) {
+            // matrix row 1 (see nwap_dp_word<.., PEEL>): H'[1][j] = max(BIAS - e_j*D, H'[1][j-1])
+            const uint2 x0 = nwap_lds64(sa);
+            sa += 8u;
+            uint32_t left = x0.y;
+            P[0] = NWAP_BIAS2;
+#pragma unroll
+            for (int j = 1; j <= LB; ++j) {
+                const uint32_t dw = nwap_viaddmin_u16x2(x0.x, nb[j - 1], 0x00010001u) * sc.neg_delta + NWAP_BIAS2;
+                left = nwap_vmaxs2(dw, left);
+                P[j] = left;
+            }
+            d0 = x0.y;
+#pragma unroll 1
+            while (sa != ea) {
+                const uint2 x = nwap_lds64(sa);
+                sa += 8u;
+                nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
+                d0 = x.y;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;     // H'[0][j]
+            d0 = NWAP_BIAS2;
+#pragma unroll 1
+            do {                                                 // la >= 1 always
+                const uint2 x = nwap_lds64(sa);
+                sa += 8u;
+                nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
+                d0 = x.y;
+            } while (sa != ea);
+        }
+        const uint32_t v = nwap_merge3(P[LB], P[LB >= 2 ? LB - 1 : LB], P[LB >= 3 ? LB - 2 : LB], c);
+        const uint32_t t = v + cur.x + kpos2;                    // halves: score + BIAS
+#if NWAP_F2_MULHI
+        uint32_t thi;                                            // t >> 16 on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF)
+        asm volatile("mul.hi.u32 %0, %1, 65536;" : "=r"(thi) : "r"(t));
+#else
+        const uint32_t thi = t >> 16;
+#endif
+        nwap_sts8(o0 + cur.y, t);
+        nwap_sts8(o1 + cur.y, thi);
+#if !NWAP_X_NOMM
+        ls.mn2 = __vmins2(ls.mn2, t);
+        ls.mx2 = __vmaxs2(ls.mx2, t);
+#endif
+#if NWAP_X_FMA
+        { uint32_t z = t;
+#pragma unroll
+          for (int q = 0; q < NWAP_X_FMA; ++q) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(z) : "r"(sc.one), "r"(sc.u2));
+          acc_hi += z; }
+#endif
+#if NWAP_X_ALU
+        { uint32_t z = t;
+#pragma unroll
+          for (int q = 0; q < NWAP_X_ALU; ++q) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(z) : "r"(sc.one), "r"(sc.u2));
+          acc_hi += z; }
+#endif
+#if NWAP_F2_DP2A
+        acc = __dp2a_lo(t, 0x0101u, acc);                        // lo + hi: at most 2 * 16 * (BIAS + 127)
+#elif NWAP_BIAS * NWAP_R + 127 * NWAP_R < 65536
+        acc += t;                                                // the low halves' sum cannot carry into the high half
+#else
+        acc += t; acc_hi += thi;
+#endif
+    }
+#if NWAP_F2_DP2A
+    ls.sum += (long long)acc - 2ll * NWAP_R * (long long)NWAP_BIAS;
+#elif NWAP_BIAS * NWAP_R + 127 * NWAP_R < 65536
+    ls.sum += (long long)(acc & 0xffffu) + (long long)(acc >> 16) - 2ll * NWAP_R * (long long)NWAP_BIAS;
+#else
+    ls.sum += (long long)(acc - (acc_hi << 16)) + (long long)acc_hi - 2ll * NWAP_R * (long long)NWAP_BIAS;
+#endif
+    ls.count += 2 * NWAP_R;
+}
+
+template <int FLAVOR, int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk_fast2(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                     const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                     const nwap_lane_cols &c, nwap_lane_stats &ls)
+{
+#if NWAP_F2_SHARED_UNPACK
+    uint32_t nbq[QMAX];                                          // one copy of the unpack code for all bodies
+    nwap_unpack_cols<FLAVOR, QMAX, QW>(w0, w1, nbq);
+#else
+    const uint32_t *nbq = nullptr;
+#endif
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_chunk_rows_fast2<(n <= QMAX ? n : 1), FLAVOR, QW>(sm, sc, w0, w1, nbq, c, ls); \
+        break;
+    switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+}
+
+
 // Tried and rejected this round (same-box A/B, evidence in profiles/r01c..r01e and git history):
 // hoisting the length dispatch out of the row loop, one symbol stream per band, dual-chain
 // chunks (4 columns per lane), a cold code family for chunks spanning >= 3 lengths.
 
-__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, uint32_t symmul, uint32_t left0, const nwap_ov_row *, int)
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, const nwap_scheme_consts &sc, uint32_t left0, const nwap_ov_row *, int)
 {
-    x.a2 = a * symmul; x.left0 = left0;
+    x.a2 = nwap_row_code(a, sc); x.left0 = left0;
 }
-__device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, uint32_t symmul, uint32_t left0, const nwap_ov_row *ov, int K)
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, const nwap_scheme_consts &sc, uint32_t left0, const nwap_ov_row *ov, int K)
 {
-    x.a2 = a * symmul; x.left0 = left0; x.pad = 0;
+    x.a2 = nwap_row_code(a, sc); x.left0 = left0; x.pad = 0;
     x.ovi = ((int)a < K && ov[a].count) ? a : NWAP_NO_OV;
 }
 
@@ -561,7 +791,7 @@ __device__ __forceinline__ void nwap_sparse_row(SM &sm, const nwap_tile_params &
     if (seg <= 0) return;
     const nwap_sparse_out &so = p.sparse;
     if (so.mode == 1 ? so.threshold > 127 : so.gmin > so.gmax) return;       // nothing can be kept
-    const int skew = m.skew;
+    const int skew = nwap_meta_skew(m, rr);
     const uint8_t *rowbase = sm.out + rr * NWAP_PITCH;           // 16-byte aligned; the segment starts at +skew
     const int nvec = (skew + seg + 15) >> 4;
     for (int v0 = 0; v0 < nvec; v0 += 32) {
@@ -730,7 +960,7 @@ k_score_tiles(const nwap_tile_params p)
             if (tid < NWAP_R) {
                 const int64_t r = rb0 + tid;
                 nwap_row_meta m;
-                m.la = 0; m.clo_off = 0; m.seglen = 0; m.rowadj = 0; m.ala2 = 0; m.skew = 0; m.g0 = 0;
+                m.la = 0; m.clo_off = 0; m.seglen = 0; m.rowadj = 0; m.ala2 = 0; m.symend = 0; m.g0 = 0;
                 if (r >= rmin && r <= rmax) {
                     int64_t clo = max(strip_lo, r + 1);
                     int64_t chi = strip_hi;
@@ -741,8 +971,9 @@ k_score_tiles(const nwap_tile_params p)
                         m.clo_off = (int)(clo - strip_lo);
                         m.seglen = (int)(chi - clo);
                         m.g0 = nwap_before_row(r, p.n) + (clo - r - 1) - p.start;
-                        m.skew = (int)((reinterpret_cast<uintptr_t>(p.out) + (uintptr_t)m.g0) & 15u);
-                        m.rowadj = tid * NWAP_PITCH + m.skew - m.clo_off;
+                        const int skew = (int)((reinterpret_cast<uintptr_t>(p.out) + (uintptr_t)m.g0) & 15u);
+                        m.rowadj = tid * NWAP_PITCH + skew - m.clo_off;
+                        m.symend = (uint32_t)__cvta_generic_to_shared(&sm.rowsym[tid][m.la]);
                         m.ala2 = (uint32_t)(sc.alpha * m.la * 65537);
                     }
                 }
@@ -759,7 +990,7 @@ k_score_tiles(const nwap_tile_params p)
                     for (int e = 0; e < 4; ++e) {
                         const uint32_t a = (v >> (8 * e)) & 0xffu;
                         if (q4 * 4 + e < la_r)           // slot [la] belongs to the boundary record
-                            nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, sc.symmul, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
+                            nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, sc, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
                                            sm.ov, p.ov_K);
                     }
                 }
@@ -818,6 +1049,13 @@ k_score_tiles(const nwap_tile_params p)
                 // two code families only where the register budget allows (the 32-wide and sparse-override
                 // instantiations would spill): there the hoisted bodies also carry the slow emit
                 constexpr bool FASTONLY = NWAP_HOIST_FASTONLY && QMAX <= 24 && !OV;
+#if NWAP_FAST2
+                if constexpr (FASTONLY && FLAVOR == 1) {
+                    if (fast && mixmode <= 2) nwap_run_chunk_fast2<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, ls);
+                    else nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
+                    continue;
+                }
+#endif
                 if (!FASTONLY || fast) nwap_run_chunk_h<FLAVOR, QMAX, QW, FASTONLY>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
                 else nwap_run_chunk<FLAVOR, QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
 #else
@@ -835,7 +1073,7 @@ k_score_tiles(const nwap_tile_params p)
             for (int rr = warp; rr < NWAP_R; rr += NWAP_WARPS) {
                 const int seg = sm.meta[rr].seglen;
                 if (seg <= 0) continue;
-                const int skew = sm.meta[rr].skew;
+                const int skew = nwap_meta_skew(sm.meta[rr], rr);
                 const uint8_t *src = sm.out + rr * NWAP_PITCH + skew;
                 int8_t *dst = p.out + sm.meta[rr].g0;
                 int head = (16 - skew) & 15;

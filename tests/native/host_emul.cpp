@@ -6,28 +6,28 @@
 #include "nwap_index.cuh"
 #include "nwap_core.cuh"
 
-template <int LB, int FLAVOR>
+template <int LB, int FLAVOR, bool PEEL = false>
 static uint32_t run_pair(const uint8_t *a, int la, const uint8_t *b0, int lb0,
                          const uint8_t *b1, int lb1, const nwap_scheme_consts &sc)
 {
     nwap_sym2 row2[256];
     for (int i = 0; i < la; ++i) {
-        row2[i].a2 = (uint32_t)a[i] * sc.symmul;
+        row2[i].a2 = nwap_row_code(a[i], sc);
         row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
 
     }
     uint32_t nb[LB];
     for (int j = 0; j < LB; ++j)
         nb[j] = nwap_pack_negb_f<FLAVOR>(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
-    return nwap_dp_pair<LB, FLAVOR>(row2, la, nb, lb0, lb1, sc);
+    return nwap_dp_pair<LB, FLAVOR, PEEL>(row2, la, nb, lb0, lb1, sc);
 }
 
-template <int FLAVOR>
+template <int FLAVOR, bool PEEL = false>
 static uint32_t dispatch(int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0,
                          const uint8_t *b1, int lb1, const nwap_scheme_consts &sc)
 {
     switch (LB) {
-#define CASE(n) case n: return run_pair<n, FLAVOR>(a, la, b0, lb0, b1, lb1, sc);
+#define CASE(n) case n: return run_pair<n, FLAVOR, PEEL>(a, la, b0, lb0, b1, lb1, sc);
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
         CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
         CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24)
@@ -43,13 +43,13 @@ static uint32_t run_pair_ov(const uint8_t *a, int la, const uint8_t *b0, int lb0
 {
     nwap_sym4 row4[256];
     for (int i = 0; i < la; ++i) {
-        row4[i].a2 = (uint32_t)a[i] * 65537u;
+        row4[i].a2 = nwap_row_code(a[i], sc);
         row4[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
         row4[i].ovi = tab[a[i]].count ? a[i] : NWAP_NO_OV;
         row4[i].pad = 0;
     }
     uint32_t nb[LB];
-    for (int j = 0; j < LB; ++j) nb[j] = nwap_pack_negb(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
+    for (int j = 0; j < LB; ++j) nb[j] = nwap_pack_negb_f<1>(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
     uint32_t P[LB + 1];
     nwap_dp_word_ov<LB, 1>(row4, la, nb, P, sc, tab);
     uint32_t lo = 0, hi = 0;
@@ -137,7 +137,7 @@ int emul_pair_scores_wide(const uint8_t *a, int la, const uint8_t *b0, int lb0, 
     nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap, 1);
     nwap_sym2 row2[NWAP_MAXLEN_WIDE + 1];
     for (int i = 0; i < la; ++i) {
-        row2[i].a2 = (uint32_t)a[i] * sc.symmul;
+        row2[i].a2 = nwap_row_code(a[i], sc);
         row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
     }
     uint8_t p0[NWAP_MAXLEN_WIDE + NWAP_WB] = {0}, p1[NWAP_MAXLEN_WIDE + NWAP_WB] = {0};
@@ -158,9 +158,11 @@ int emul_pair_scores(int flavor, int LB, const uint8_t *a, int la, const uint8_t
 {
     if (LB < 1 || LB > 32 || lb0 > LB || lb1 > LB || la < 1 || lb0 < 1 || lb1 < 1) return -1;
     if (flavor == 2 && !nwap_flavor2_ok(match, mismatch)) return -3;
-    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap, flavor);
+    // flavor 11: the default cell (FLAVOR 1) with the peeled first matrix row
+    nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap, flavor == 11 ? 1 : flavor);
     uint32_t v = flavor == 0 ? dispatch<0>(LB, a, la, b0, lb0, b1, lb1, sc)
                : flavor == 1 ? dispatch<1>(LB, a, la, b0, lb0, b1, lb1, sc)
+               : flavor == 11 ? dispatch<1, true>(LB, a, la, b0, lb0, b1, lb1, sc)
                              : dispatch<2>(LB, a, la, b0, lb0, b1, lb1, sc);
     *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
     *s1 = nwap_unbias(v >> 16, la, lb1, sc);

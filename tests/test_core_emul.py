@@ -50,7 +50,7 @@ def _random_scheme(rng, q):
             return m, x, g
 
 
-@pytest.mark.parametrize("flavor", [0, 1, 2])
+@pytest.mark.parametrize("flavor", [0, 1, 2, 11])
 def test_packed_recurrence_matches_oracle(emul, flavor):
     rng = random.Random(1234 + flavor)
     for _ in range(6000):
@@ -106,7 +106,7 @@ def test_packed_recurrence_extreme_schemes(emul):
             a = np.array([rng.randrange(3) for _ in range(la)], dtype=np.uint8)
             b0 = np.array([rng.randrange(3) for _ in range(lb0)], dtype=np.uint8)
             b1 = np.array([rng.randrange(3) for _ in range(lb1)], dtype=np.uint8)
-            for fl in (0, 1, 2):
+            for fl in (0, 1, 2, 11):
                 if fl == 2 and m < x:
                     continue
                 s0, s1 = ctypes.c_int(), ctypes.c_int()
