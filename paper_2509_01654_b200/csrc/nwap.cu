@@ -127,6 +127,7 @@ struct nwap_ctx {
     int64_t sort_table_cap = 0;
     unsigned long long *d_kept = nullptr;
     short2 *d_kbounds = nullptr;
+    short2 *d_ftab = nullptr;          // normalised filter: 512 per-length score bounds (nwap_keep_params::dtab)
 };
 
 // Two device slabs, two streams and four events: everything nwap_score_range_host needs to overlap
@@ -512,7 +513,7 @@ void nwap_destroy(nwap_ctx *c)
     cudaDeviceSynchronize();             // nothing may still be reading the store or writing the slabs
     dev_free(c->d_ids); dev_free(c->d_lens); dev_free(c->d_sim); dev_free(c->d_stats); dev_free(c->d_ov); dev_free(c->d_etab);
     dev_free(c->d_counter); dev_free(c->d_block_counts); dev_free(c->d_total);
-    dev_free(c->d_kept); dev_free(c->d_kbounds);
+    dev_free(c->d_kept); dev_free(c->d_kbounds); dev_free(c->d_ftab);
     cudaFree(c->d_keys); cudaFree(c->d_sort_table);
     if (c->pipe) {                       // back to the device cache for the next context
         std::lock_guard<std::mutex> lock(g_cache_mutex);
@@ -660,7 +661,7 @@ int nwap_payload_stats(nwap_ctx *c, const int8_t *payload_dev, int64_t count, nw
 }
 
 static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start, int64_t end, int mode,
-                          const nwap_keep_params &kp, int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap,
+                          const nwap_keep_params &kp_in, int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap,
                           int64_t *count_host, int32_t *degree_dev, cudaStream_t st)
 {
     if (!c || !count_host) return fail(NWAP_EINVAL, "null argument");
@@ -672,6 +673,18 @@ static int compact_common(nwap_ctx *c, const int8_t *payload_dev, int64_t start,
     if (count == 0) return NWAP_OK;
     if (!payload_dev) return fail(NWAP_EINVAL, "null payload");
     ON_DEVICE(c->device);
+    nwap_keep_params kp = kp_in;
+    kp.dtab = nullptr;
+    if (mode == 1) {
+        if (!c->d_ftab) CK(dev_alloc(&c->d_ftab, sizeof(short2) * 512));
+        short2 hb[512];
+        for (int m = 0; m < 256; ++m) {
+            hb[m] = make_short2(kp.smin[m], kp.smax[m]);
+            hb[256 + m] = make_short2(kp.rmin[m], kp.rmax[m]);
+        }
+        CK(cudaMemcpyAsync(c->d_ftab, hb, sizeof hb, cudaMemcpyHostToDevice, st));   // pageable source: staged before return
+        kp.dtab = c->d_ftab;
+    }
     // blocks tile the 16-byte aligned window that contains the slice (k_compact_*: nwap_cmp_first)
     const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload_dev) & 15u);
     const int64_t nblocks = (lead + count + NWAP_CMP_BLOCK - 1) / NWAP_CMP_BLOCK;
@@ -844,7 +857,7 @@ int nwap_hist_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, 
     const int64_t runs = (count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
     if (c->qmax <= 100) {
         // joint (max length, score) bins: no per-edge division, 26 KB of shared memory at 24 symbols
-        const size_t smem = sizeof(unsigned int) * 256 * (size_t)(c->qmax + 1);
+        const size_t smem = sizeof(unsigned int) * (size_t)(256 + nwap_joint_mul(c->qmax)) * (size_t)(c->qmax + 1);
         CK(cudaFuncSetAttribute(k_hist_norm_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / (smem + 1024)));
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((runs + 511) / 512, (int64_t)c->sm_count * per_sm));

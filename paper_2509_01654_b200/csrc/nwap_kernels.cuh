@@ -213,6 +213,14 @@ struct nwap_block_rows {
 };
 
 __device__ __forceinline__ void nwap_block_rows_init(nwap_block_rows *br, const nwap_keep_params &kp, int64_t k_block,
+                                                     int64_t count);
+__device__ __forceinline__ void nwap_block_rows_sync(nwap_block_rows *br, const nwap_keep_params &kp, int64_t k_block,
+                                                     int64_t count)
+{
+    nwap_block_rows_init(br, kp, k_block, count);
+    __syncthreads();
+}
+__device__ __forceinline__ void nwap_block_rows_init(nwap_block_rows *br, const nwap_keep_params &kp, int64_t k_block,
                                                      int64_t count)
 {
     if (threadIdx.x == 0) {
@@ -227,14 +235,13 @@ __device__ __forceinline__ void nwap_block_rows_init(nwap_block_rows *br, const 
     }
 }
 
-template <int MODE>
-__device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__restrict__ payload, int64_t count,
-                                                             int64_t k_first, const nwap_keep_params &kp,
-                                                             uint4 (&vec)[NWAP_CMP_VEC], const short2 *bounds,
-                                                             const short2 *rbounds = nullptr,
-                                                             const nwap_block_rows *br = nullptr)
+// MODE 1, phase A: load the thread's 64 window bytes and mark the CANDIDATES from the payload alone -- a score outside
+// [gmin, gmax] (the loosest bounds over all lengths) cannot be kept whatever the word lengths are.  Needs nothing but
+// the payload and two scalars, so a block whose threads find no candidate is done without any index recovery, bounds
+// table or barrier (selective filters: almost every block).
+__device__ __forceinline__ unsigned long long nwap_window_load(const int8_t *__restrict__ payload, int64_t count,
+                                                               int64_t k_first, uint4 (&vec)[NWAP_CMP_VEC])
 {
-    unsigned long long bits = 0;
     if (k_first >= count || k_first + NWAP_CMP_PER_THREAD <= 0) {
 #pragma unroll
         for (int v = 0; v < NWAP_CMP_VEC; ++v) vec[v] = make_uint4(0u, 0u, 0u, 0u);
@@ -242,33 +249,15 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
     }
 #pragma unroll
     for (int v = 0; v < NWAP_CMP_VEC; ++v) vec[v] = nwap_cmp_load(payload, count, k_first + 16 * v);
-    // validity mask of this thread's 64 window bytes
-    unsigned long long valid = ~0ull;
+    unsigned long long valid = ~0ull;                            // validity mask of this thread's 64 window bytes
     if (k_first < 0) valid &= ~0ull << (int)(-k_first);
     if (k_first + NWAP_CMP_PER_THREAD > count) valid &= ~0ull >> (int)(k_first + NWAP_CMP_PER_THREAD - count);
-    if (MODE == 0) {
-        const int t = kp.threshold;
-        if (t > 127) return 0;
-        if (t <= -128) return valid;
-        const uint32_t T = (uint32_t)(t + 128);
-        const uint32_t tl_rep = (T & 0x7fu) * 0x01010101u;
-        const bool th = (T & 0x80u) != 0;
-#pragma unroll
-        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
-            const uint32_t w[4] = {vec[v].x, vec[v].y, vec[v].z, vec[v].w};
-            unsigned b16 = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) b16 |= nwap_ge_bits4(w[q], tl_rep, th) << (4 * q);
-            bits |= (unsigned long long)b16 << (16 * v);
-        }
-        return bits & valid;
-    }
-    // MODE 1: lo <= 100.0*score/max(len_r, len_c) <= hi (graph.py:96-98) through the per-length score
-    // bounds in shared memory; (r, c) walks the triangle
-    // candidates first, from the payload alone: a score outside [gmin, gmax] (the loosest bounds over all lengths)
-    // cannot be kept whatever the word lengths are.  Selective filters reject most edges here, 4 per SWAR step,
-    // before any index recovery or length fetch.
-    if (kp.gmin > kp.gmax) return 0;
+    return valid;
+}
+__device__ __forceinline__ unsigned long long nwap_cand_bits(const nwap_keep_params &kp, const uint4 (&vec)[NWAP_CMP_VEC],
+                                                             unsigned long long valid)
+{
+    if (valid == 0 || kp.gmin > kp.gmax) return 0;
     unsigned long long cand = 0;
     {
         const uint32_t Tlo = (uint32_t)(kp.gmin + 128);                 // gmin >= -128
@@ -293,15 +282,29 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
         }
         cand &= valid;
     }
+    return cand;
+}
+
+// MODE 1, phase B: the exact keep-mask of the candidates -- lo <= 100.0*score/max(len_r, len_c) <= hi (graph.py:96-98)
+// through the per-length score bounds in shared memory; (r, c) walks the triangle.
+__device__ __forceinline__ unsigned long long nwap_keep_eval(int64_t count, int64_t k_first, const nwap_keep_params &kp,
+                                                             const uint4 (&vec)[NWAP_CMP_VEC], unsigned long long cand,
+                                                             unsigned long long valid, const short2 *bounds,
+                                                             const short2 *rbounds, const nwap_block_rows *br)
+{
+    unsigned long long bits = 0;
     if (cand == 0) return 0;
     const int64_t kb = max(k_first, (int64_t)0);
     const int64_t ke = min(k_first + (int64_t)NWAP_CMP_PER_THREAD, count) - 1;       // last live edge of this thread
+    // the block's one or two rows were recovered once (nwap_block_rows_init); a thread places itself by comparisons
     int64_t r = -1;
-    if (br && br->r0 >= 0) {
+    if (br->r0 >= 0) {
         if (ke < br->next1) r = br->r0;
         else if (kb >= br->next1 && ke < br->next2) r = br->r0 + 1;
     }
-    if (r >= 0) {
+    const bool one_row = r >= 0;
+    if (!one_row) r = nwap_row_of(kp.start + kb, kp.n);
+    if (one_row && __popcll(cand) <= 8) {
         // all live edges of this thread lie in row r: its own length tightens the candidate bounds (m >= len_r),
         // and the few survivors fetch their column length one byte each
         const int lr1 = (int)kp.lens[r];
@@ -320,7 +323,6 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
         }
         return bits;
     }
-    r = nwap_row_of(kp.start + kb, kp.n);
     int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
     int lr = (int)kp.lens[r];
     if (valid == ~0ull && c + NWAP_CMP_PER_THREAD <= kp.n) {
@@ -360,6 +362,42 @@ __device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__res
     return bits;
 }
 
+template <int MODE>
+__device__ __forceinline__ unsigned long long nwap_keep_bits(const int8_t *__restrict__ payload, int64_t count,
+                                                             int64_t k_first, const nwap_keep_params &kp,
+                                                             uint4 (&vec)[NWAP_CMP_VEC], const short2 *bounds,
+                                                             const short2 *rbounds = nullptr,
+                                                             nwap_block_rows *br = nullptr)
+{
+    unsigned long long bits = 0;
+    if (MODE == 0) {
+        const unsigned long long valid = nwap_window_load(payload, count, k_first, vec);
+        if (valid == 0) return 0;
+        const int t = kp.threshold;
+        if (t > 127) return 0;
+        if (t <= -128) return valid;
+        const uint32_t T = (uint32_t)(t + 128);
+        const uint32_t tl_rep = (T & 0x7fu) * 0x01010101u;
+        const bool th = (T & 0x80u) != 0;
+#pragma unroll
+        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
+            const uint32_t w[4] = {vec[v].x, vec[v].y, vec[v].z, vec[v].w};
+            unsigned b16 = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) b16 |= nwap_ge_bits4(w[q], tl_rep, th) << (4 * q);
+            bits |= (unsigned long long)b16 << (16 * v);
+        }
+        return bits & valid;
+    }
+    // MODE 1: the payload loads are issued first; the block's rows are recovered by thread 0 while they are in flight
+    // (the barrier inside nwap_block_rows_sync), then candidates from the payload alone, then the exact test
+    const unsigned long long valid1 = nwap_window_load(payload, count, k_first, vec);
+    nwap_block_rows_sync(br, kp, k_first - (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD, count);
+    const unsigned long long cand = nwap_cand_bits(kp, vec, valid1);
+    if (cand == 0) return 0;
+    return nwap_keep_eval(count, k_first, kp, vec, cand, valid1, bounds, rbounds, br);
+}
+
 // first window byte of (block, thread), as an edge offset relative to payload[0] (may be negative)
 __device__ __forceinline__ int64_t nwap_cmp_first(const int8_t *payload)
 {
@@ -372,19 +410,15 @@ __global__ void __launch_bounds__(NWAP_CMP_THREADS)
 k_compact_count(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, long long *block_counts,
                 unsigned long long *group_totals)
 {
-    __shared__ short2 bounds[MODE == 1 ? 256 : 1], rbounds[MODE == 1 ? 256 : 1];
+    // MODE 1: the per-length score bounds live in a 2 KB device table (kp.dtab: [0, 256) per m, [256, 512) per row
+    // length) read through L1 by the few threads that hold a candidate.  (Staging them in shared memory from the
+    // kernel parameters cost a 32-way serialised constant load per warp and a barrier per 16 KB block: 1.2 TB/s.)
     __shared__ nwap_block_rows brows;
-    if (MODE == 1) {
-        bounds[threadIdx.x] = make_short2(kp.smin[threadIdx.x], kp.smax[threadIdx.x]);     // NWAP_CMP_THREADS == 256
-        rbounds[threadIdx.x] = make_short2(kp.rmin[threadIdx.x], kp.rmax[threadIdx.x]);
-        nwap_block_rows_init(&brows, kp, nwap_cmp_first(payload) - (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD, count);
-        __syncthreads();
-    }
     uint4 vec[NWAP_CMP_VEC];
-    int kept = __popcll(nwap_keep_bits<MODE>(payload, count, nwap_cmp_first(payload), kp, vec, bounds, rbounds, &brows));
+    const int kept = __popcll(nwap_keep_bits<MODE>(payload, count, nwap_cmp_first(payload), kp, vec, kp.dtab, kp.dtab + 256, &brows));
     __shared__ int wsum[NWAP_CMP_THREADS / 32];
-    kept = __reduce_add_sync(0xffffffffu, kept);
-    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = kept;
+    const int wkept = __reduce_add_sync(0xffffffffu, kept);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = wkept;
     __syncthreads();
     if (threadIdx.x == 0) {
         int tot = 0;
@@ -468,17 +502,10 @@ k_compact_write(const int8_t *__restrict__ payload, int64_t count, const nwap_ke
     const long long off0 = block_offsets[blockIdx.x];
     const long long off1 = (int64_t)blockIdx.x + 1 < nblocks ? block_offsets[blockIdx.x + 1] : *total;
     if (off1 == off0) return;
-    __shared__ short2 bounds[MODE == 1 ? 256 : 1], rbounds[MODE == 1 ? 256 : 1];
-    __shared__ nwap_block_rows brows;
     const int64_t k_first = nwap_cmp_first(payload);
-    if (MODE == 1) {
-        bounds[threadIdx.x] = make_short2(kp.smin[threadIdx.x], kp.smax[threadIdx.x]);
-        rbounds[threadIdx.x] = make_short2(kp.rmin[threadIdx.x], kp.rmax[threadIdx.x]);
-        nwap_block_rows_init(&brows, kp, k_first - (int64_t)threadIdx.x * NWAP_CMP_PER_THREAD, count);
-        __syncthreads();
-    }
+    __shared__ nwap_block_rows brows;
     uint4 vec[NWAP_CMP_VEC];
-    const unsigned long long bits = nwap_keep_bits<MODE>(payload, count, k_first, kp, vec, bounds, rbounds, &brows);
+    const unsigned long long bits = nwap_keep_bits<MODE>(payload, count, k_first, kp, vec, kp.dtab, kp.dtab + 256, &brows);
     const int kept = __popcll(bits);
     // exclusive scan of `kept` over the block
     __shared__ int wtot[NWAP_CMP_THREADS / 32];
@@ -701,6 +728,8 @@ k_hist_normalized(const int8_t *__restrict__ payload, int64_t count, const nwap_
 // of the lengths as byte-parallel integer ops -- and map each occupied (m, score) bin to floor(100*score / m) ONCE
 // per CTA at the end, in exact integer arithmetic (store.py:357-361).  Needs mmax <= 127 (byte-parallel max on
 // 7-bit lengths) and (mmax + 1) KB of shared memory; longer words use k_hist_normalized.
+// swizzle multiplier of the joint histogram: the largest odd j in {9, 5, 3, 1} with mmax * j < 256
+__host__ __device__ inline int nwap_joint_mul(int mmax) { return mmax <= 28 ? 9 : mmax <= 51 ? 5 : mmax <= 85 ? 3 : 1; }
 __device__ __forceinline__ uint32_t nwap_bytemax7(uint32_t a, uint32_t b)        // per-byte max, all bytes < 128
 {
     const uint32_t ge = (((a | 0x80808080u) - b) >> 7) & 0x01010101u;             // 1 where a >= b
@@ -720,8 +749,12 @@ __global__ void __launch_bounds__(512)
 k_hist_norm_joint(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, unsigned long long *counts,
                   int mmax)
 {
-    extern __shared__ unsigned int jbins[];              // [(mmax + 1) * 256], key = m << 8 | (score + 128)
-    const int nb = (mmax + 1) * 256;
+    // bin address = m * JS + (score + 128), JS = 256 + jmul: with a stride of 256 words every m lands in the same bank
+    // for a given score and the warp's atomics serialise 3x (ncu: 130 M bank conflicts per 2 Gi edges, L1 at 99 %);
+    // 265 = 9 mod 32 spreads the ~25 hot (m, score) pairs over distinct banks
+    extern __shared__ unsigned int jbins[];              // [(mmax + 1) * JS]
+    const int jmul = nwap_joint_mul(mmax), JS = 256 + jmul;
+    const int nb = (mmax + 1) * JS;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) jbins[b] = 0;
     __syncthreads();
     const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload) & 15u);
@@ -745,11 +778,13 @@ k_hist_norm_joint(const int8_t *__restrict__ payload, int64_t count, const nwap_
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t x = w[q] ^ 0x80808080u;                       // score + 128 per byte
                     const uint32_t m4 = nwap_bytemax7(L[4 * v + q], lr4);
-                    // key j = {x byte j, m4 byte j, 0, 0}: selector nibbles 8|k replicate the (clear) sign of a length byte
-                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xcc40u)], 1u);
-                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xdd51u)], 1u);
-                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xee62u)], 1u);
-                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xff73u)], 1u);
+                    const uint32_t s4 = m4 * (uint32_t)jmul;                     // per byte (mmax * jmul < 256: no carry): the swizzle term
+                    // key j = {x byte j, m4 byte j, 0, 0} (selector nibbles 8|k replicate the clear sign of a length
+                    // byte) = m * 256 + score + 128; adding byte j of s4 makes it m * JS + score + 128
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xcc40u) + nwap_prmt(s4, 0u, 0x4440u)], 1u);
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xdd51u) + nwap_prmt(s4, 0u, 0x4441u)], 1u);
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xee62u) + nwap_prmt(s4, 0u, 0x4442u)], 1u);
+                    atomicAdd(&jbins[nwap_prmt(x, m4, 0xff73u) + nwap_prmt(s4, 0u, 0x4443u)], 1u);
                 }
             }
             continue;
@@ -766,17 +801,19 @@ k_hist_norm_joint(const int8_t *__restrict__ payload, int64_t count, const nwap_
                 if (k >= 0 && k < count) {
                     const int m = max(lr, (int)kp.lens[c]);
                     const uint32_t sb = ((w[j >> 2] >> (8 * (j & 3))) & 0xffu) ^ 0x80u;
-                    atomicAdd(&jbins[(m << 8) | (int)sb], 1u);
+                    atomicAdd(&jbins[m * JS + (int)sb], 1u);
                     if (++c == kp.n) { ++r; c = r + 1; lr = (int)kp.lens[min(r, kp.n - 1)]; }
                 }
             }
         }
     }
     __syncthreads();
-    for (int b = 256 + threadIdx.x; b < nb; b += blockDim.x) {          // m = 0 never occurs (every word has >= 1 symbol)
+    for (int b = JS + threadIdx.x; b < nb; b += blockDim.x) { // m = 0 never occurs (every word has >= 1 symbol)
         const unsigned int h = jbins[b];
         if (h) {
-            const int m = b >> 8, num = 100 * ((b & 255) - 128);
+            const int m = b / JS, sb = b - m * JS;
+            if (sb > 255) continue;                                         // padding words of the swizzled layout
+            const int num = 100 * (sb - 128);
             int qv = num / m;
             if (num % m != 0 && num < 0) --qv;                          // floor division
             atomicAdd(&counts[qv - NWAP_NHIST_OFFSET], (unsigned long long)h);

@@ -66,6 +66,7 @@ struct nwap_keep_params {
     // MODE 1: loosest bounds over the lengths m >= l (up to the longest word): what a score in a row whose word has
     // l symbols must satisfy whatever the column is, since m = max(len_r, len_c) >= len_r.  Empty: rmin > rmax.
     int8_t rmin[256], rmax[256];
+    const short2 *dtab;      // MODE 1: the same bounds on the device: [m] = (smin, smax), [256 + l] = (rmin, rmax)
 };
 
 // host side of the table above
