@@ -80,11 +80,15 @@ nwap_tile_kernel_t nwap_tile_kernel(int family, int qclass)
     }
 }
 
-size_t nwap_tile_smem_bytes(int family)
+size_t nwap_tile_smem_bytes(int family, int K)
 {
     switch (family) {
     case 3: return sizeof(nwap_tile_smem_t<1>);
-    case 4: return sizeof(nwap_tile_smem_t<2>);
+    case 4: {
+        // the K x K table is the struct's last member: K = 0 asks for the largest alphabet
+        const size_t tab = K > 0 ? (((size_t)K * (size_t)K + 15u) & ~size_t(15)) : (size_t)NWAP_OV_MAXK * NWAP_OV_MAXK;
+        return offsetof(nwap_tile_smem_t<2>, etab) + std::max<size_t>(16, tab);
+    }
     case 5: case 7: return sizeof(nwap_tile_smem_t<0, NWAP_MAXLEN_WIDE>);
     default: return sizeof(nwap_tile_smem_t<0>);
     }
@@ -276,8 +280,9 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     const bool sym_ok = fast_ok && !c->general && nwap_flavor2_ok(c->match, c->mismatch);
     // PACKED3 (2 DPX + IMAD + IADD) is ~8 % faster than PACKED (2 DPX + 2 IMAD) and ~14 % faster than PACKED_SYM
     // (2 DPX + IADD3: one issue fewer, but IADD3 shares the DPX pipe): profiles/r01f_ab_packed_sym.txt
-    // override tables: the table-driven cell beats the sparse-correction cell whenever the alphabet fits shared
-    // memory, so `auto` takes it first.  A uniform scheme never leaves the packed kernel: the preflight admits at
+    // override tables: the table-driven cell (6.1 TCUPS whatever the table holds, two CTAs per SM up to ~100 symbols)
+    // is at least as fast as the sparse-correction cell (5.1-6.3 TCUPS, profiles/r02b_overrides.txt) whenever the
+    // alphabet fits shared memory, so `auto` takes it first.  A uniform scheme never leaves the packed kernel: the preflight admits at
     // most 64 symbols per word (gap -1, engine.py:83-90), which the wide build covers.
     if (variant == NWAP_VARIANT_AUTO)
         variant = tab_ok ? NWAP_VARIANT_PACKED_TAB : (fast_ok || wide_ok) ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
@@ -334,7 +339,13 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     if (sparse) p.sparse = *sparse;
     else memset(&p.sparse, 0, sizeof p.sparse);
 
-    const int occ = std::max(1, c->occ_tiles[family * 3 + qclass]);
+    int occ = std::max(1, c->occ_tiles[family * 3 + qclass]);
+    const size_t smem_bytes = nwap_tile_smem_bytes(family, tab ? c->K : 0);
+    if (tab) {          // the table-driven flavour's footprint depends on the alphabet: two CTAs per SM up to ~100 symbols
+        int o = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, nwap_tile_kernel(family, qclass), NWAP_THREADS, smem_bytes));
+        occ = std::max(1, o);
+    }
     const int64_t slots = (int64_t)c->sm_count * occ;
     // bands per group: as large as possible (amortises the per-unit sort) while
     // leaving >= 24 units per resident CTA for dynamic balance.
@@ -353,7 +364,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     p.us = us; p.unit_begin = ubeg; p.unit_count = ucount;
     const int64_t grid = std::min<int64_t>(slots, ucount);
     CK(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
-    nwap_tile_kernel(family, qclass)<<<(unsigned)grid, NWAP_THREADS, nwap_tile_smem_bytes(family), st>>>(p);
+    nwap_tile_kernel(family, qclass)<<<(unsigned)grid, NWAP_THREADS, smem_bytes, st>>>(p);
     g_launches++;
     CK(cudaGetLastError());
     if (want_hist && out_dev) {

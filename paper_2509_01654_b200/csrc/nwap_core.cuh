@@ -325,68 +325,158 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
 }
 
 // ---- sparse overrides (ScoringScheme.overrides, reference aligner.py:51-65) -----------------
-// sim(a, b) = uniform(a, b) + delta(a, b) with delta != 0 for at most NWAP_MAX_OV partners b of
-// any symbol a.  For a matrix row whose symbol has partners (b_k, delta_k) the diagonal term is
-//     dw = diag - e*D + sum_k delta_k * [b_j == b_k]
-//        = diag - e*D + sum_k (delta_k - delta_k * e_k),   e_k = min(b_k + (-b_j), 1)
-// i.e. one extra DPX compare + IMAD per partner slot and one add of dsum = sum_k delta_k.
-// Rows whose symbol has no partner run the plain cell.
-#define NWAP_MAX_OV 3
-struct nwap_ov_row {                 // one row of the per-symbol override table
-    uint32_t b2[NWAP_MAX_OV];        // partner symbol as a row code (FLAVOR 1: 256 - b in both halves; unused slot: anything)
+// sim(a, b) = uniform(a, b) + delta(a, b) with delta != 0 for at most NWAP_MAX_OV partners b of any symbol a
+// (a itself may be one of them).  For a matrix row whose symbol has partners (p_k, delta_k) the diagonal term is
+//     dw = diag - e*D + sum_k delta_k * [b_j == p_k]
+//        = diag - e*D - sum_k delta_k * e_k + dsum,   e_k = min(p_k - b_j, 1),  dsum = sum_k delta_k:
+// one extra DPX compare + IMAD per partner -- and a constant.  The constant is removed by a ROW potential:
+// with G_i = -(dsum of matrix rows 1..i) and H''[i][j] = H'[i][j] + G_i,
+//     H''[i][j] = max(H''[i-1][j-1] - e*D - sum_k delta_k*e_k,  H''[i-1][j] + (u - dsum_i),  H''[i][j-1]),
+// i.e. the row's `up` addend and its boundary value H''[i][0] = BIAS + i*u + G_i come from the staged row record
+// (they did anyway) and the score fix-up of the row word absorbs -G_la.  Rows whose symbol has no partner run the
+// plain cell; rows with one / two partners run 6 / 8 instructions per packed cell instead of 4.
+#define NWAP_MAX_OV 2
+#ifndef NWAP_OV_PRE
+#define NWAP_OV_PRE 0
+#endif
+#ifndef NWAP_OV_PREFETCH
+#define NWAP_OV_PREFETCH 0
+#endif
+#ifndef NWAP_OV_ONE
+#define NWAP_OV_ONE 1               // 1: rows with one partner have their own 6-instruction cell (else they run the 8-instruction one)
+#endif
+struct nwap_ov_row {                 // one row of the per-symbol override table (32 bytes)
+    uint32_t b2[NWAP_MAX_OV];        // partner symbol as a row code (FLAVOR 1: 256 - p in both halves; unused slot: anything)
     uint32_t nd[NWAP_MAX_OV];        // (uint32)(-delta_k)     (unused slot: 0)
-    uint32_t dsum;                   // (uint32)(sum_k delta_k) * 65537 ... packed for both halves
+    int32_t dsum;                    // sum_k delta_k
     uint32_t count;                  // number of used slots
+    uint32_t pad[2];
 };
-struct nwap_sym4 { uint32_t a2, left0, ovi, pad; };   // ovi = symbol index into the table, or NWAP_NO_OV
-#define NWAP_NO_OV 0xffffffffu
+// staged record of one matrix row of an override scheme (one LDS.128) and the per-symbol partner table the
+// override rows read on top of it (kept apart so that the staged rows stay small: two CTAs must fit one SM)
+struct alignas(16) nwap_sym8 {
+    uint32_t a2, left0, ui2, ov;     // row code, H''[i][0], (u - dsum_i) * 65537, 0 = no partner else symbol << 2 | count
+};
+struct alignas(16) nwap_ov_part {
+    uint32_t p0, nd0, p1, nd1;       // partners' row codes and -delta
+};
 
-template <int LB, int FLAVOR>
-NWAP_HD void nwap_dp_row_ov(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
-                            uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc, const nwap_ov_row &ov)
+// One score-matrix row with N partners, software-pipelined like nwap_dp_row (the diagonal term of cell j+1 is formed
+// from the old P[j] before P[j] is overwritten).
+template <int LB, int N>
+NWAP_HD void nwap_dp_row_ov(const nwap_sym8 &xr, const nwap_ov_part &y, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                            uint32_t d0, const nwap_scheme_consts &sc)
 {
-    uint32_t left = left0;
-    uint32_t diag = d0;
+    struct { uint32_t a2, left0, ui2, p0, nd0, p1, nd1; } x = {xr.a2, xr.left0, xr.ui2, y.p0, y.nd0, y.p1, y.nd1};
+#if NWAP_OV_PRE
+    // the partner terms do not depend on the rolling row: all LB of them first (independent instructions), then
+    // the plain cell with one more addend
+    uint32_t t[LB];
+#pragma unroll
+    for (int j = 0; j < LB; ++j) {
+        t[j] = nwap_viaddmin_u16x2(x.p0, nb[j], 0x00010001u) * x.nd0;
+        if (N > 1) t[j] = nwap_viaddmin_u16x2(x.p1, nb[j], 0x00010001u) * x.nd1 + t[j];
+    }
+    uint32_t left = x.left0;
+    uint32_t dw = nwap_viaddmin_u16x2(x.a2, nb[0], 0x00010001u) * sc.neg_delta + d0 + t[0];
 #pragma unroll
     for (int j = 1; j <= LB; ++j) {
-        uint32_t dw = nwap_viaddmin_u16x2(a2, nb[j - 1], 0x00010001u) * sc.neg_delta + diag;
-#pragma unroll
-        for (int k = 0; k < NWAP_MAX_OV; ++k)
-            dw = nwap_viaddmin_u16x2(ov.b2[k], nb[j - 1], 0x00010001u) * ov.nd[k] + dw;
-        dw += ov.dsum;
-        diag = P[j];
-        const uint32_t upu = P[j] + sc.u2;
-        const uint32_t cur = nwap_vimax3_s16x2(dw, upu, left);
+        uint32_t dw_next = 0;
+        if (j < LB) dw_next = nwap_viaddmin_u16x2(x.a2, nb[j], 0x00010001u) * sc.neg_delta + P[j] + t[j];
+        const uint32_t cur = nwap_vimax3_s16x2(dw, P[j] + x.ui2, left);
         P[j] = cur;
         left = cur;
+        dw = dw_next;
     }
+#else
+    uint32_t left = x.left0;
+    uint32_t dw = nwap_viaddmin_u16x2(x.a2, nb[0], 0x00010001u) * sc.neg_delta + d0;
+    dw = nwap_viaddmin_u16x2(x.p0, nb[0], 0x00010001u) * x.nd0 + dw;
+    if (N > 1) dw = nwap_viaddmin_u16x2(x.p1, nb[0], 0x00010001u) * x.nd1 + dw;
+#pragma unroll
+    for (int j = 1; j <= LB; ++j) {
+        uint32_t dw_next = 0;
+        if (j < LB) {
+            dw_next = nwap_viaddmin_u16x2(x.a2, nb[j], 0x00010001u) * sc.neg_delta + P[j];
+            dw_next = nwap_viaddmin_u16x2(x.p0, nb[j], 0x00010001u) * x.nd0 + dw_next;
+            if (N > 1) dw_next = nwap_viaddmin_u16x2(x.p1, nb[j], 0x00010001u) * x.nd1 + dw_next;
+        }
+        const uint32_t cur = nwap_vimax3_s16x2(dw, P[j] + x.ui2, left);
+        P[j] = cur;
+        left = cur;
+        dw = dw_next;
+    }
+#endif
 }
 
 template <int LB, int FLAVOR>
-NWAP_HD void nwap_dp_word_ov(const nwap_sym4 *row_sym4, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
-                             const nwap_scheme_consts &sc, const nwap_ov_row *ovtab)
+NWAP_HD void nwap_dp_word_ov(const nwap_sym8 *rec, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                             const nwap_scheme_consts &sc, const nwap_ov_part *parts)
 {
 #pragma unroll
     for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
     uint32_t d0 = NWAP_BIAS2;
-    const nwap_sym4 *s = row_sym4, *e = row_sym4 + la;
+    const nwap_sym8 *s = rec, *e = rec + la;
+    // the record of the next matrix row is fetched a row ahead: the dispatch on its partner count would otherwise
+    // wait for the load at every row (rec[la] is readable: the staged rows hold one record more than the longest word)
+#if NWAP_OV_PREFETCH
+    nwap_sym8 nxt = *s;
+#endif
 #pragma unroll 1
     do {
-        const nwap_sym4 x = *s++;
-        if (x.ovi == NWAP_NO_OV) nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
-        else nwap_dp_row_ov<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc, ovtab[x.ovi]);
+#if NWAP_OV_PREFETCH
+        const nwap_sym8 x = nxt;
+        nxt = *++s;
+#else
+        const nwap_sym8 x = *s++;
+#endif
+        if (x.ov == 0) nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+        else {
+            const nwap_ov_part y = parts[x.ov >> 2];
+#if NWAP_OV_ONE
+            if ((x.ov & 3u) == 1u) nwap_dp_row_ov<LB, 1>(x, y, nb, P, d0, sc);
+            else
+#endif
+            nwap_dp_row_ov<LB, 2>(x, y, nb, P, d0, sc);
+        }
         d0 = x.left0;
     } while (s != e);
 }
 
+// Staged records of one row word (a[0..la)): row codes, partners, and the row potential folded into the boundary
+// values and `up` addends.  Returns sum_i dsum(a_i) = -G_la, which the caller adds to the row word's score fix-up.
+NWAP_HD int nwap_stage_row_ov(const uint8_t *a, int la, const nwap_ov_row *tab, int K, const nwap_scheme_consts &sc,
+                              nwap_sym8 *rec)
+{
+    const int u = (int)(int16_t)(sc.u2h & 0xffffu);
+    int gsum = 0;
+    for (int i = 0; i < la; ++i) {
+        const uint32_t sym = a[i];
+        nwap_sym8 x;
+        x.a2 = nwap_row_code(sym, sc);
+        x.ov = 0;
+        int ds = 0;
+        if ((int)sym < K && tab[sym].count) {
+            x.ov = (sym << 2) | tab[sym].count;
+            ds = tab[sym].dsum;
+        }
+        gsum += ds;
+        x.left0 = NWAP_BIAS2 + (uint32_t)((i + 1) * u - gsum) * 65537u;
+        x.ui2 = (uint32_t)(u - ds) * 65537u;
+        rec[i] = x;
+    }
+    return gsum;
+}
+
 // Host-side construction of the override table from a dense K x K similarity table
 // (reference engine.py:110-117).  Returns false when some symbol has more than NWAP_MAX_OV
-// partners (the scheme then goes to the table-driven generic kernel).
+// partners (the scheme then goes to the table-driven cell or the generic kernel).
 inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatch, nwap_ov_row *out)
 {
     for (int a = 0; a < K; ++a) {
         nwap_ov_row r;
         for (int k = 0; k < NWAP_MAX_OV; ++k) { r.b2[k] = 0; r.nd[k] = 0; }
+        r.pad[0] = r.pad[1] = 0;
         int cnt = 0, dsum = 0;
         for (int b = 0; b < K; ++b) {
             const int delta = (int)sim[a * K + b] - (a == b ? match : mismatch);
@@ -397,7 +487,7 @@ inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatc
             dsum += delta;
             ++cnt;
         }
-        r.dsum = (uint32_t)(dsum * 65537);
+        r.dsum = dsum;
         r.count = (uint32_t)cnt;
         out[a] = r;
     }

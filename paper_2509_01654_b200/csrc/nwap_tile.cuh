@@ -161,7 +161,7 @@ __device__ __forceinline__ int nwap_meta_skew(const nwap_row_meta &m, int rr) { 
 // ---------------------------------------------------------------------------
 #define NWAP_OV_MAXK 128               // largest alphabet the sparse-override table holds in shared memory
 template <int MODE> struct nwap_sym_of { typedef nwap_sym2 type; };
-template <> struct nwap_sym_of<1> { typedef nwap_sym4 type; };
+template <> struct nwap_sym_of<1> { typedef nwap_sym8 type; };
 
 // MODE 0: uniform scheme, 1: sparse overrides (per-symbol correction rows), 2: dense table (K x K bytes of M - sim)
 // MAXLEN: longest word the instantiation accepts (32, or 64 for the block-wise wide build)
@@ -170,8 +170,7 @@ struct nwap_tile_smem_t {
     alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
     typedef typename nwap_sym_of<MODE>::type sym_t;
     alignas(16) sym_t rowsym[NWAP_R][MAXLEN + 1];                // {a*65537, H'[i+1][0] (, override row)} per matrix row
-    alignas(16) nwap_ov_row ov[MODE == 1 ? NWAP_OV_MAXK : 1];       // per-symbol override table (sparse-override mode)
-    alignas(16) uint8_t etab[MODE == 2 ? NWAP_OV_MAXK * NWAP_OV_MAXK : 16];   // dense-table mode
+    alignas(16) nwap_ov_part ov[MODE == 1 ? NWAP_OV_MAXK : 1];      // per-symbol partner table (sparse-override mode)
     alignas(16) nwap_row_meta meta[NWAP_R + 1];                     // one readable record past the band (row prefetch)
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
     uint8_t clen[NWAP_C];         // their lengths
@@ -183,6 +182,9 @@ struct nwap_tile_smem_t {
     int mn, mx;
     int ncols;
     int next_chunk;
+    // dense-table mode: K x K bytes of M - sim.  LAST member: the launch sizes the dynamic shared memory to the
+    // alphabet actually used (nwap_tile_smem_bytes), so that tables of up to ~100 symbols leave room for two CTAs per SM
+    alignas(16) uint8_t etab[MODE == 2 ? NWAP_OV_MAXK * NWAP_OV_MAXK : 16];
 };
 
 typedef nwap_tile_smem_t<0> nwap_tile_smem;
@@ -304,19 +306,19 @@ struct nwap_false { __device__ constexpr operator bool() const { return false; }
 // strip) selects per lane among all columns.
 template <int LB, int FLAVOR>
 __device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym2 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
-                                                 const nwap_scheme_consts &sc, const nwap_ov_row *)
+                                                 const nwap_scheme_consts &sc, const nwap_ov_part *)
 {
     nwap_dp_word<LB, FLAVOR>(sym, la, nb, P, sc);
 }
 template <int LB, int FLAVOR>
-__device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym4 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
-                                                 const nwap_scheme_consts &sc, const nwap_ov_row *ovtab)
+__device__ __forceinline__ void nwap_dp_word_sel(const nwap_sym8 *sym, int la, const uint32_t *nb, uint32_t (&P)[LB + 1],
+                                                 const nwap_scheme_consts &sc, const nwap_ov_part *parts)
 {
-    nwap_dp_word_ov<LB, FLAVOR>(sym, la, nb, P, sc, ovtab);
+    nwap_dp_word_ov<LB, FLAVOR>(sym, la, nb, P, sc, parts);
 }
 
 template <int LB, int FLAVOR, class SYM>
-__device__ __forceinline__ void nwap_row_dp(const SYM *sym, const nwap_ov_row *ovtab, int la, const uint32_t *nb,
+__device__ __forceinline__ void nwap_row_dp(const SYM *sym, const nwap_ov_part *ovtab, int la, const uint32_t *nb,
                                             int l0, int l1, const nwap_scheme_consts &sc, uint32_t &v, uint32_t &vm1,
                                             uint32_t &vm2, bool deep)
 {
@@ -724,14 +726,13 @@ __device__ __forceinline__ void nwap_run_chunk_fast2(int LB, SM &sm, const nwap_
 // hoisting the length dispatch out of the row loop, one symbol stream per band, dual-chain
 // chunks (4 columns per lane), a cold code family for chunks spanning >= 3 lengths.
 
-__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, const nwap_scheme_consts &sc, uint32_t left0, const nwap_ov_row *, int)
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, const nwap_scheme_consts &sc, uint32_t left0, const nwap_ov_part *, int)
 {
     x.a2 = nwap_row_code(a, sc); x.left0 = left0;
 }
-__device__ __forceinline__ void nwap_stage_sym(nwap_sym4 &x, uint32_t a, const nwap_scheme_consts &sc, uint32_t left0, const nwap_ov_row *ov, int K)
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym8 &, uint32_t, const nwap_scheme_consts &, uint32_t, const nwap_ov_part *, int)
 {
-    x.a2 = nwap_row_code(a, sc); x.left0 = left0; x.pad = 0;
-    x.ovi = ((int)a < K && ov[a].count) ? a : NWAP_NO_OV;
+    // override schemes stage whole rows (nwap_stage_row_ov, one thread per row: the row potential is a prefix sum)
 }
 
 // One chunk whose longest word exceeds the register-resident row: block-wise DP (nwap_dp_blocks), per-lane
@@ -860,7 +861,7 @@ __device__ __forceinline__ void nwap_sparse_row(SM &sm, const nwap_tile_params &
 // CMP: sparse-output mode (p.sparse): the flush stage scans the staged scores for kept edges; the dense store
 // happens only when p.out is non-NULL.
 template <int FLAVOR, int QMAX, bool OV, bool WIDE = false, bool CMP = false>
-__global__ void __launch_bounds__(NWAP_THREADS, (((OV || FLAVOR == 3) && QMAX > 24) ? 1 : NWAP_MINB))   // the 32-wide sparse-override / table builds need > 96 registers
+__global__ void __launch_bounds__(NWAP_THREADS, ((OV || (FLAVOR == 3 && QMAX > 24)) ? 1 : NWAP_MINB))   // sparse-override builds run one CTA per SM (two lose: profiles/r02b_overrides.txt); the 32-wide table build needs > 96 registers
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -884,9 +885,12 @@ k_score_tiles(const nwap_tile_params p)
         for (int b = tid; b < 256; b += NWAP_THREADS) sm.kbounds[b] = p.sparse.bounds[b];
     const nwap_sparse_consts skc = nwap_make_sparse_consts(p.sparse);
     if (OV) {
-        const uint32_t *src = reinterpret_cast<const uint32_t *>(p.ov_table);
-        uint32_t *dst = reinterpret_cast<uint32_t *>(sm.ov);
-        for (int w = tid; w < p.ov_K * (int)(sizeof(nwap_ov_row) / 4); w += NWAP_THREADS) dst[w] = src[w];
+        for (int k = tid; k < p.ov_K; k += NWAP_THREADS) {
+            const nwap_ov_row t = p.ov_table[k];
+            nwap_ov_part y;
+            y.p0 = t.b2[0]; y.nd0 = t.nd[0]; y.p1 = t.b2[1]; y.nd1 = t.nd[1];
+            sm.ov[k] = y;
+        }
     }
     nwap_lane_stats ls;
     ls.mn2 = 0x7fff7fffu; ls.mx2 = 0u; ls.sum = 0; ls.count = 0;
@@ -976,12 +980,17 @@ k_score_tiles(const nwap_tile_params p)
                         m.rowadj = tid * NWAP_PITCH + skew - m.clo_off;
                         m.symend = (uint32_t)__cvta_generic_to_shared(&sm.rowsym[tid][m.la]);
                         m.ala2 = (uint32_t)(sc.alpha * m.la * 65537);
+                        if (OV) {
+                            const int gsum = nwap_stage_row_ov(p.ids + r * p.qpad, m.la, p.ov_table, p.ov_K, sc,
+                                                               reinterpret_cast<nwap_sym8 *>(&sm.rowsym[tid][0]));
+                            m.ala2 = (uint32_t)((sc.alpha * m.la + gsum) * 65537);
+                        }
                     }
                 }
                 sm.meta[tid] = m;
             }
             // stage row symbols, packed a*65537, with the row boundary values (4 symbols per item)
-            for (int item = tid; item < NWAP_R * (SYMLEN / 4); item += NWAP_THREADS) {
+            for (int item = tid; !OV && item < NWAP_R * (SYMLEN / 4); item += NWAP_THREADS) {
                 const int rr = item / (SYMLEN / 4), q4 = item % (SYMLEN / 4);
                 const int64_t r = rb0 + rr;
                 if (q4 < (WIDE ? (p.qpad >> 2) : QW) && r >= rmin && r <= rmax) {
@@ -1127,7 +1136,7 @@ k_score_tiles(const nwap_tile_params p)
 typedef void (*nwap_tile_kernel_t)(const nwap_tile_params);
 #define NWAP_TILE_FAMILIES 8
 nwap_tile_kernel_t nwap_tile_kernel(int family, int qclass);
-size_t nwap_tile_smem_bytes(int family);
+size_t nwap_tile_smem_bytes(int family, int K = 0);
 nwap_tile_kernel_t nwap_tiles_f0f2(int family, int qclass);
 nwap_tile_kernel_t nwap_tiles_f1(int qclass);
 nwap_tile_kernel_t nwap_tiles_ov(int qclass);

@@ -39,19 +39,16 @@ static uint32_t dispatch(int LB, const uint8_t *a, int la, const uint8_t *b0, in
 
 template <int LB>
 static uint32_t run_pair_ov(const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,
-                            const nwap_scheme_consts &sc, const nwap_ov_row *tab)
+                            const nwap_scheme_consts &sc, const nwap_ov_row *tab, int K, int *gsum)
 {
-    nwap_sym4 row4[256];
-    for (int i = 0; i < la; ++i) {
-        row4[i].a2 = nwap_row_code(a[i], sc);
-        row4[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
-        row4[i].ovi = tab[a[i]].count ? a[i] : NWAP_NO_OV;
-        row4[i].pad = 0;
-    }
+    nwap_sym8 rec[256];
+    *gsum = nwap_stage_row_ov(a, la, tab, K, sc, rec);
     uint32_t nb[LB];
     for (int j = 0; j < LB; ++j) nb[j] = nwap_pack_negb_f<1>(j < lb0 ? b0[j] : 0u, j < lb1 ? b1[j] : 0u);
+    static nwap_ov_part parts[256];
+    for (int k = 0; k < K; ++k) { parts[k].p0 = tab[k].b2[0]; parts[k].nd0 = tab[k].nd[0]; parts[k].p1 = tab[k].b2[1]; parts[k].nd1 = tab[k].nd[1]; }
     uint32_t P[LB + 1];
-    nwap_dp_word_ov<LB, 1>(row4, la, nb, P, sc, tab);
+    nwap_dp_word_ov<LB, 1>(rec, la, nb, P, sc, parts);
     uint32_t lo = 0, hi = 0;
     for (int j = 1; j <= LB; ++j) {
         if (j == lb0) lo = P[j] & 0xffffu;
@@ -116,16 +113,17 @@ int emul_pair_scores_ov(int LB, const uint8_t *a, int la, const uint8_t *b0, int
     if (!nwap_build_ov_table(sim, K, match, mismatch, tab)) return -2;
     nwap_scheme_consts sc = nwap_make_consts(match, mismatch, gap);
     uint32_t v = 0;
+    int gsum = 0;
     switch (LB) {
-#define CASE(n) case n: v = run_pair_ov<n>(a, la, b0, lb0, b1, lb1, sc, tab); break;
+#define CASE(n) case n: v = run_pair_ov<n>(a, la, b0, lb0, b1, lb1, sc, tab, K, &gsum); break;
         CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
         CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
         CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23) CASE(24)
         CASE(25) CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31) CASE(32)
 #undef CASE
     }
-    *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
-    *s1 = nwap_unbias(v >> 16, la, lb1, sc);
+    *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc) + gsum;          // the row potential's share of the fix-up
+    *s1 = nwap_unbias(v >> 16, la, lb1, sc) + gsum;
     return 0;
 }
 

@@ -146,7 +146,7 @@ def test_sparse_override_rows_match_oracle(emul):
         assert rc == 0
         checked += 1
         assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim, g), orc.c_nw_score(a, b1, sim, g)), (m, x, g, ov)
-    assert checked > 3500 and dense < 100
+    assert checked > 3500 and dense < 300          # at most NWAP_MAX_OV = 2 partners per symbol run this cell
 
 
 def test_dense_table_rows_match_oracle(emul):

@@ -404,9 +404,9 @@ def test_random_schemes_all_variants():
 
 
 def test_sparse_override_schemes_on_the_packed_kernel():
-    """ScoringScheme.overrides: random sparse override sets (<= 3 partners per symbol) must give the same
-    bytes on the packed sparse-override kernel, the generic kernel and the oracle; a dense table is
-    refused by the packed kernel and served by the generic one."""
+    """ScoringScheme.overrides: random sparse override sets must give the same bytes on the packed sparse-override
+    kernel (at most 2 partners per symbol: NWAP_MAX_OV), the generic kernel and the oracle; a denser table is
+    refused by the sparse-override cell and served by the table-driven / generic one."""
     rng = np.random.default_rng(77)
     for trial in range(10):
         q = int(rng.integers(4, 25))
@@ -427,8 +427,18 @@ def test_sparse_override_schemes_on_the_packed_kernel():
         scheme = nw.ScoringScheme(m, x, g, overrides=ov)
         P = nw.num_edges(n)
         ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P, threads=4)
+        partners = {}
+        for (a_, b_), val in ov.items():
+            if val != (m if a_ == b_ else x):
+                partners.setdefault(a_, set()).add(b_)
+                partners.setdefault(b_, set()).add(a_)
+        sparse = all(len(v_) <= 2 for v_ in partners.values())
         with NwapContext(ids, lens, scheme) as ctx:
             for v in ("auto", "packed3", "simple"):
+                if v == "packed3" and not sparse:
+                    with pytest.raises(ValueError, match="packed kernel"):
+                        _score(ctx, 0, P, v)
+                    continue
                 got, st = _score(ctx, 0, P, v, want_hist=(trial % 2 == 0))
                 assert np.array_equal(got, ref), (trial, v, (m, x, g), ov)
                 assert st[:4] == (rsum, rmin, rmax, P)
