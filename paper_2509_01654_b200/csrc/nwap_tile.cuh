@@ -525,13 +525,16 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
 #define NWAP_FAST2 1
 #endif
 #ifndef NWAP_F2_PEEL_MAXLB
-#define NWAP_F2_PEEL_MAXLB 8
+#define NWAP_F2_PEEL_MAXLB 0
 #endif
 #ifndef NWAP_F2_DP2A
 #define NWAP_F2_DP2A 0
 #endif
 #ifndef NWAP_F2_SHARED_UNPACK
 #define NWAP_F2_SHARED_UNPACK 0
+#endif
+#ifndef NWAP_F2_DUFF_MAXLB
+#define NWAP_F2_DUFF_MAXLB 8
 #endif
 #ifndef NWAP_F2_LEANHEAD
 #define NWAP_F2_LEANHEAD 0
@@ -646,6 +649,28 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
                 nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
                 d0 = x.y;
             }
+        } else if (LB <= NWAP_F2_DUFF_MAXLB) {
+            // two matrix rows per loop trip (one pointer bump, test, branch and no boundary move per two rows); a
+            // word of odd length enters at the second copy
+#pragma unroll
+            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
+            d0 = NWAP_BIAS2;
+            if ((ea - sa) & 8u) { sa -= 8u; goto second_row; }
+#pragma unroll 1
+            do {
+                {
+                    const uint2 x = nwap_lds64(sa);
+                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
+                    d0 = x.y;
+                }
+            second_row:
+                {
+                    const uint2 x = nwap_lds64(sa + 8u);
+                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
+                    d0 = x.y;
+                }
+                sa += 16u;
+            } while (sa != ea);
         } else {
 #pragma unroll
             for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;     // H'[0][j]
