@@ -12,7 +12,8 @@
 // with e = [a_i != b_j] in {0,1}, D = match - mismatch, u = 2*gap - match,
 // boundary H'[0][j] = BIAS, H'[i][0] = BIAS + i*u.
 // Per packed cell (2 DP cells) that is
-//     e   = VIADDMNMX.U16x2 (a + (-b), min 1)        ALU pipe
+//     e   = VIADDMNMX.U16x2 (row code + column code, min 1)   ALU pipe   (codes: nwap_pack_negb_f; the sum is b - a
+//                                                                        mod 2^16, zero iff the symbols are equal)
 //     dw  = IMAD            (e * (-D) + diag)        FMA pipe  (packed-safe: halves stay in [0,2^15))
 //     cur = VIMNMX3.S16x2   (dw, up_plus_u, left)    ALU pipe
 //     upu = IMAD            (cur * 1 + u*65537)      FMA pipe  (next row's up + u)
@@ -215,20 +216,6 @@ NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
 // row's boundary value (BIAS2 + (i+1)*u2, the same for every word), fetched together.
 struct nwap_sym2 { uint32_t a2, left0; };
 
-// Build-time micro-variants (A/B-tested on the GPU, see profiles/):
-//   NWAP_SYM64    1: fetch {symbol, boundary} with one 8-byte load; 0: load the symbol, add u2
-//   NWAP_PREFETCH 1: load the next matrix row's symbol before working on the current one
-#ifndef NWAP_SYM64
-#define NWAP_SYM64 1
-#endif
-#ifndef NWAP_PREFETCH
-#define NWAP_PREFETCH 0
-#endif
-//   NWAP_DUFF_MAXLB n: length bodies up to n run two matrix rows per loop trip (0 = off)
-#ifndef NWAP_DUFF_MAXLB
-#define NWAP_DUFF_MAXLB 0
-#endif
-
 // PEEL (FLAVOR 1 only): matrix row 1 is peeled.  Every H'[0][j] is BIAS, so its diagonal term is BIAS - e*D, and
 // its up term BIAS + u equals the row's boundary value H'[1][0] the left chain starts from, i.e. it is absorbed:
 // H'[1][j] = max(BIAS - e_j*D, H'[1][j-1]) -- three instructions per cell instead of four and no initialisation of
@@ -270,58 +257,12 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
         } while (s != e);
         return;
     }
-#if NWAP_DUFF_MAXLB > 0
-    if (LB <= NWAP_DUFF_MAXLB) {
-        // two matrix rows per loop trip; an odd word enters at the second copy (the update is in place, so
-        // both copies are the same code on the same registers)
-        if (la & 1) goto second_row;
-#pragma unroll 1
-        do {
-            {
-                const nwap_sym2 x = *s++;
-                nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
-                d0 = x.left0;
-            }
-        second_row:
-            {
-                const nwap_sym2 x = *s++;
-                nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
-                d0 = x.left0;
-            }
-        } while (s != e);
-        return;
-    }
-#endif
-#if NWAP_PREFETCH
-    nwap_sym2 x = *s;
 #pragma unroll 1
     do {                                                    // la >= 1 always
-        ++s;
-        const nwap_sym2 cur = x;
-        x = *s;                                             // one element past the word is readable padding
-#if NWAP_SYM64
-        const uint32_t left0 = cur.left0;
-#else
-        const uint32_t left0 = d0 + sc.u2;
-#endif
-        nwap_dp_row<LB, FLAVOR>(cur.a2, nb, P, d0, left0, sc);
-        d0 = left0;
+        const nwap_sym2 x = *s++;                           // {symbol, boundary} in one 8-byte load
+        nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
+        d0 = x.left0;
     } while (s != e);
-#else
-#pragma unroll 1
-    do {                                                    // la >= 1 always
-#if NWAP_SYM64
-        const nwap_sym2 x = *s++;
-        const uint32_t left0 = x.left0;
-        const uint32_t a2 = x.a2;
-#else
-        const uint32_t a2 = (s++)->a2;
-        const uint32_t left0 = d0 + sc.u2;
-#endif
-        nwap_dp_row<LB, FLAVOR>(a2, nb, P, d0, left0, sc);
-        d0 = left0;
-    } while (s != e);
-#endif
 }
 
 // ---- sparse overrides (ScoringScheme.overrides, reference aligner.py:51-65) -----------------
@@ -336,12 +277,6 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
 // (they did anyway) and the score fix-up of the row word absorbs -G_la.  Rows whose symbol has no partner run the
 // plain cell; rows with one / two partners run 6 / 8 instructions per packed cell instead of 4.
 #define NWAP_MAX_OV 2
-#ifndef NWAP_OV_PRE
-#define NWAP_OV_PRE 0
-#endif
-#ifndef NWAP_OV_PREFETCH
-#define NWAP_OV_PREFETCH 0
-#endif
 #ifndef NWAP_OV_ONE
 #define NWAP_OV_ONE 1               // 1: rows with one partner have their own 6-instruction cell (else they run the 8-instruction one)
 #endif
@@ -368,27 +303,6 @@ NWAP_HD void nwap_dp_row_ov(const nwap_sym8 &xr, const nwap_ov_part &y, const ui
                             uint32_t d0, const nwap_scheme_consts &sc)
 {
     struct { uint32_t a2, left0, ui2, p0, nd0, p1, nd1; } x = {xr.a2, xr.left0, xr.ui2, y.p0, y.nd0, y.p1, y.nd1};
-#if NWAP_OV_PRE
-    // the partner terms do not depend on the rolling row: all LB of them first (independent instructions), then
-    // the plain cell with one more addend
-    uint32_t t[LB];
-#pragma unroll
-    for (int j = 0; j < LB; ++j) {
-        t[j] = nwap_viaddmin_u16x2(x.p0, nb[j], 0x00010001u) * x.nd0;
-        if (N > 1) t[j] = nwap_viaddmin_u16x2(x.p1, nb[j], 0x00010001u) * x.nd1 + t[j];
-    }
-    uint32_t left = x.left0;
-    uint32_t dw = nwap_viaddmin_u16x2(x.a2, nb[0], 0x00010001u) * sc.neg_delta + d0 + t[0];
-#pragma unroll
-    for (int j = 1; j <= LB; ++j) {
-        uint32_t dw_next = 0;
-        if (j < LB) dw_next = nwap_viaddmin_u16x2(x.a2, nb[j], 0x00010001u) * sc.neg_delta + P[j] + t[j];
-        const uint32_t cur = nwap_vimax3_s16x2(dw, P[j] + x.ui2, left);
-        P[j] = cur;
-        left = cur;
-        dw = dw_next;
-    }
-#else
     uint32_t left = x.left0;
     uint32_t dw = nwap_viaddmin_u16x2(x.a2, nb[0], 0x00010001u) * sc.neg_delta + d0;
     dw = nwap_viaddmin_u16x2(x.p0, nb[0], 0x00010001u) * x.nd0 + dw;
@@ -406,7 +320,6 @@ NWAP_HD void nwap_dp_row_ov(const nwap_sym8 &xr, const nwap_ov_part &y, const ui
         left = cur;
         dw = dw_next;
     }
-#endif
 }
 
 template <int LB, int FLAVOR>
@@ -419,17 +332,9 @@ NWAP_HD void nwap_dp_word_ov(const nwap_sym8 *rec, int la, const uint32_t *nb, u
     const nwap_sym8 *s = rec, *e = rec + la;
     // the record of the next matrix row is fetched a row ahead: the dispatch on its partner count would otherwise
     // wait for the load at every row (rec[la] is readable: the staged rows hold one record more than the longest word)
-#if NWAP_OV_PREFETCH
-    nwap_sym8 nxt = *s;
-#endif
 #pragma unroll 1
     do {
-#if NWAP_OV_PREFETCH
-        const nwap_sym8 x = nxt;
-        nxt = *++s;
-#else
         const nwap_sym8 x = *s++;
-#endif
         if (x.ov == 0) nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
         else {
             const nwap_ov_part y = parts[x.ov >> 2];

@@ -517,44 +517,21 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
 // word lengths (mixmode <= 2) -- everything else goes through the compact per-row-dispatch family.  Compared with
 // nwap_chunk_rows_h it executes fewer instructions per row word:
 //   * no deep select and no mixmode tests: the final cell is always merged from the last three columns;
-//   * the negated column symbols are unpacked inside the length body (LB of them, not QMAX);
-//   * the packed sum is one IDP.2A (lo + hi into a 32-bit accumulator) instead of two adds;
-//   * row metadata and row symbols are walked by pointer (meta[] has one readable record past the band);
-//   * bodies up to NWAP_F2_PEEL_MAXLB peel the first matrix row (nwap_dp_word<.., PEEL>).
+//   * the column codes are unpacked inside the length body (LB of them, not QMAX: three PRMT per two columns);
+//   * shared memory is addressed through 32-bit shared-window addresses, rows and metadata walked by pointer
+//     (meta[] has one readable record past the band: the next row's record is fetched a row ahead);
+//   * bodies up to NWAP_F2_DUFF_MAXLB run two matrix rows per loop trip (6 control instructions per two rows
+//     instead of 5 per row; beyond LB 8 the doubled body loses to instruction-cache misses);
+//   * NWAP_F2_PEEL_MAXLB > 0 peels the first matrix row of short bodies instead (nwap_dp_word<.., PEEL>; +0.8 % at
+//     LB <= 8, not additive with the two-row loop: off).  A/B record: profiles/r02a_ab_fast2.txt.
 #ifndef NWAP_FAST2
 #define NWAP_FAST2 1
 #endif
 #ifndef NWAP_F2_PEEL_MAXLB
 #define NWAP_F2_PEEL_MAXLB 0
 #endif
-#ifndef NWAP_F2_DP2A
-#define NWAP_F2_DP2A 0
-#endif
-#ifndef NWAP_F2_SHARED_UNPACK
-#define NWAP_F2_SHARED_UNPACK 0
-#endif
 #ifndef NWAP_F2_DUFF_MAXLB
 #define NWAP_F2_DUFF_MAXLB 8
-#endif
-#ifndef NWAP_F2_LEANHEAD
-#define NWAP_F2_LEANHEAD 0
-#endif
-#ifndef NWAP_F2_KPOS_REG
-#define NWAP_F2_KPOS_REG 0
-#endif
-#ifndef NWAP_F2_MULHI
-#define NWAP_F2_MULHI 0
-#endif
-// sensitivity experiments only (never in a shipped build): drop the min/max update, add n FMA-pipe / ALU-pipe
-// instructions per row word
-#ifndef NWAP_X_NOMM
-#define NWAP_X_NOMM 0
-#endif
-#ifndef NWAP_X_FMA
-#define NWAP_X_FMA 0
-#endif
-#ifndef NWAP_X_ALU
-#define NWAP_X_ALU 0
 #endif
 // shared-window loads by 32-bit address: one induction variable serves both the load and the loop test (with
 // generic pointers ptxas keeps two copies of it, one per use)
@@ -583,48 +560,28 @@ __device__ __forceinline__ void nwap_sts8(uint32_t addr, uint32_t v)
 
 template <int LB, int FLAVOR, int QW, class SM>
 __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_consts &sc, const uint32_t (&w0)[QW],
-                                                      const uint32_t (&w1)[QW], const uint32_t *nbq,
-                                                      const nwap_lane_cols &c, nwap_lane_stats &ls)
+                                                      const uint32_t (&w1)[QW], const nwap_lane_cols &c,
+                                                      nwap_lane_stats &ls)
 {
     constexpr bool PEEL = LB <= NWAP_F2_PEEL_MAXLB && FLAVOR == 1;
     uint32_t nb[LB];
-#if NWAP_F2_SHARED_UNPACK
-#pragma unroll
-    for (int j = 0; j < LB; ++j) nb[j] = nbq[j];
-#else
     nwap_unpack_cols<FLAVOR, LB, QW>(w0, w1, nb);
-#endif
     uint32_t acc = 0, acc_hi = 0;
     const uint32_t out_s = (uint32_t)__cvta_generic_to_shared(sm.out);
     const uint32_t o0 = out_s + c.off0, o1 = out_s + c.off1;
-    uint32_t kpos2 = c.kpos2;
-#if NWAP_F2_KPOS_REG
-    asm volatile("" : "+r"(kpos2));                              // keep it in a register (else it is rebuilt per row)
-#endif
+    const uint32_t kpos2 = c.kpos2;
     uint32_t sym_s = (uint32_t)__cvta_generic_to_shared(&sm.rowsym[0][0]);
     uint32_t meta_s = (uint32_t)__cvta_generic_to_shared(&sm.meta[0]);
     constexpr uint32_t SYM_PITCH = sizeof(sm.rowsym[0]);
     constexpr uint32_t META_PITCH = sizeof(nwap_row_meta);
-#if NWAP_F2_LEANHEAD
-    uint32_t ea_next = nwap_lds32(meta_s + 4u);
-#else
     uint4 nxt = nwap_lds128(meta_s);
-#endif
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
-#if NWAP_F2_LEANHEAD
-        // the loop bound is fetched a row ahead; {ala2, rowadj} are fetched now and used after the matrix rows
-        const uint32_t ea = ea_next;
-        const uint2 cur = nwap_lds64(meta_s + 8u);
-        ea_next = nwap_lds32(meta_s + META_PITCH + 4u);          // meta[] has one readable record past the band
-        meta_s += META_PITCH;
-#else
         // the whole 16-byte record {la, symend, ala2, rowadj} is fetched a row ahead
         const uint32_t ea = nxt.y;
         const uint2 cur = make_uint2(nxt.z, nxt.w);
         meta_s += META_PITCH;
         nxt = nwap_lds128(meta_s);                               // meta[] has one readable record past the band
-#endif
         uint32_t P[LB + 1];
         uint32_t sa = sym_s;
         sym_s += SYM_PITCH;
@@ -685,45 +642,14 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
         }
         const uint32_t v = nwap_merge3(P[LB], P[LB >= 2 ? LB - 1 : LB], P[LB >= 3 ? LB - 2 : LB], c);
         const uint32_t t = v + cur.x + kpos2;                    // halves: score + BIAS
-#if NWAP_F2_MULHI
-        uint32_t thi;                                            // t >> 16 on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF)
-        asm volatile("mul.hi.u32 %0, %1, 65536;" : "=r"(thi) : "r"(t));
-#else
         const uint32_t thi = t >> 16;
-#endif
         nwap_sts8(o0 + cur.y, t);
         nwap_sts8(o1 + cur.y, thi);
-#if !NWAP_X_NOMM
         ls.mn2 = __vmins2(ls.mn2, t);
         ls.mx2 = __vmaxs2(ls.mx2, t);
-#endif
-#if NWAP_X_FMA
-        { uint32_t z = t;
-#pragma unroll
-          for (int q = 0; q < NWAP_X_FMA; ++q) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(z) : "r"(sc.one), "r"(sc.u2));
-          acc_hi += z; }
-#endif
-#if NWAP_X_ALU
-        { uint32_t z = t;
-#pragma unroll
-          for (int q = 0; q < NWAP_X_ALU; ++q) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(z) : "r"(sc.one), "r"(sc.u2));
-          acc_hi += z; }
-#endif
-#if NWAP_F2_DP2A
-        acc = __dp2a_lo(t, 0x0101u, acc);                        // lo + hi: at most 2 * 16 * (BIAS + 127)
-#elif NWAP_BIAS * NWAP_R + 127 * NWAP_R < 65536
-        acc += t;                                                // the low halves' sum cannot carry into the high half
-#else
-        acc += t; acc_hi += thi;
-#endif
+        acc += t; acc_hi += thi;                                 // packed sums, separated once per chunk
     }
-#if NWAP_F2_DP2A
-    ls.sum += (long long)acc - 2ll * NWAP_R * (long long)NWAP_BIAS;
-#elif NWAP_BIAS * NWAP_R + 127 * NWAP_R < 65536
-    ls.sum += (long long)(acc & 0xffffu) + (long long)(acc >> 16) - 2ll * NWAP_R * (long long)NWAP_BIAS;
-#else
     ls.sum += (long long)(acc - (acc_hi << 16)) + (long long)acc_hi - 2ll * NWAP_R * (long long)NWAP_BIAS;
-#endif
     ls.count += 2 * NWAP_R;
 }
 
@@ -732,15 +658,9 @@ __device__ __forceinline__ void nwap_run_chunk_fast2(int LB, SM &sm, const nwap_
                                                      const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
                                                      const nwap_lane_cols &c, nwap_lane_stats &ls)
 {
-#if NWAP_F2_SHARED_UNPACK
-    uint32_t nbq[QMAX];                                          // one copy of the unpack code for all bodies
-    nwap_unpack_cols<FLAVOR, QMAX, QW>(w0, w1, nbq);
-#else
-    const uint32_t *nbq = nullptr;
-#endif
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
-        if (n <= QMAX) nwap_chunk_rows_fast2<(n <= QMAX ? n : 1), FLAVOR, QW>(sm, sc, w0, w1, nbq, c, ls); \
+        if (n <= QMAX) nwap_chunk_rows_fast2<(n <= QMAX ? n : 1), FLAVOR, QW>(sm, sc, w0, w1, c, ls);      \
         break;
     switch (LB) { NWAP_CASES_1_32 default: break; }
 #undef NWAP_CASE
