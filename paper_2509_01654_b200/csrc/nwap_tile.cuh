@@ -180,7 +180,8 @@ struct nwap_tile_smem_t {
     long long sum;
     long long count;
     int mn, mx;
-    int ncols;
+    int ncols;                    // sorted columns of the unit: [0, nclean) by length, longest first; [nclean, ncols) unsorted
+    int nclean;
     int next_chunk;
     // dense-table mode: K x K bytes of M - sim.  LAST member: the launch sizes the dynamic shared memory to the
     // alphabet actually used (nwap_tile_smem_bytes), so that tables of up to ~100 symbols leave room for two CTAs per SM
@@ -869,6 +870,11 @@ k_score_tiles(const nwap_tile_params p)
         }
         const int kbase = tid * PER;
         const int win_lo = (int)(cwin_lo - strip_lo), win_hi = (int)(strip_hi - strip_lo);
+        // In the strip that holds the unit's own rows (the diagonal strip) the columns up to the unit's last row are
+        // valid for some of its rows only.  They are sorted BEHIND all the others (bin 0), so that every chunk of the
+        // clean part [0, nclean) is valid for every row of every band of the unit and takes the fast path; the few
+        // chunks behind it (at most gb * 16 columns) take the path with per-lane range checks.
+        const int dirty_hi = (int)max((int64_t)0, min((int64_t)NWAP_C, grow0 + (int64_t)p.us.gb * NWAP_R - strip_lo));
         // zero the lengths of columns outside the window (and clamp, defensively)
 #pragma unroll
         for (int e = 0; e < PER; ++e) {
@@ -881,13 +887,15 @@ k_score_tiles(const nwap_tile_params p)
 #pragma unroll
         for (int e = 0; e < PER; ++e) {
             const int len = (int)nwap_byte_of(lw, e);
-            if (len) atomicAdd(&sm.bins[warp][len], 1);
+            if (len) atomicAdd(&sm.bins[warp][kbase + e < dirty_hi ? 0 : len], 1);
         }
         __syncthreads();
         if (tid == 0) {
             int run = 0;
             for (int len = MAXL; len >= 1; --len)
                 for (int w = 0; w < NWAP_WARPS; ++w) { int cnt = sm.bins[w][len]; sm.bins[w][len] = run; run += cnt; }
+            sm.nclean = run;
+            for (int w = 0; w < NWAP_WARPS; ++w) { int cnt = sm.bins[w][0]; sm.bins[w][0] = run; run += cnt; }
             sm.ncols = run;
         }
         __syncthreads();
@@ -895,7 +903,7 @@ k_score_tiles(const nwap_tile_params p)
         for (int e = 0; e < PER; ++e) {
             const int len = (int)nwap_byte_of(lw, e);
             if (len) {
-                const int pos = atomicAdd(&sm.bins[warp][len], 1);
+                const int pos = atomicAdd(&sm.bins[warp][kbase + e < dirty_hi ? 0 : len], 1);
                 sm.cols[pos] = (uint16_t)(kbase + e);
                 sm.clen[pos] = (uint8_t)len;
             }
@@ -952,17 +960,16 @@ k_score_tiles(const nwap_tile_params p)
             }
             if (tid == 0) sm.next_chunk = 0;
             __syncthreads();
-            // simple band: all R rows present and each covers the whole sorted column window, i.e. the band lies
-            // entirely to the left of the strip (every row r has r + 1 <= strip_lo, so its columns start at the
-            // strip's first column) and neither end of the launch range clips one of its rows.  Evaluated by
-            // every thread from launch scalars: no extra barrier, nothing read back from shared memory.
+            // simple band: all R rows present and neither end of the launch range clips one of them; every row then
+            // covers the whole CLEAN part of the sorted columns (columns beyond the unit's last row: in a strip to the
+            // right of the unit's rows that is every column).  Evaluated by every thread from launch scalars: no
+            // extra barrier, nothing read back from shared memory.
             const bool clip_first = p.r_first >= rb0 && p.r_first < rb0 + NWAP_R && p.c_start > strip_lo;
             const bool clip_last = p.r_last >= rb0 && p.r_last < rb0 + NWAP_R && p.c_end + 1 < strip_hi;
-            const bool band_simple = rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax &&
-                                     rb0 + NWAP_R - 1 < strip_lo && !clip_first && !clip_last;
+            const bool band_simple = rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax && !clip_first && !clip_last;
 
             // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
-            const int ncols = sm.ncols;
+            const int ncols = sm.ncols, nclean = sm.nclean;
             for (;;) {
                 int item = 0;
                 if (lane == 0) item = atomicAdd(&sm.next_chunk, 1);
@@ -971,10 +978,14 @@ k_score_tiles(const nwap_tile_params p)
                 if (kc >= ncols) break;
                 // register width of the chunk: its longest word, optionally rounded up to a multiple of
                 // NWAP_LBSTEP (fewer distinct length bodies in flight; the 3-level merge covers the slack)
-                const int LB = min(((int)sm.clen[kc] + NWAP_LBSTEP - 1) / NWAP_LBSTEP * NWAP_LBSTEP, MAXL);
                 const int ka = kc + 2 * lane, kb = ka + 1;
                 const bool va = ka < ncols, vb = kb < ncols;
-                const int la_ = va ? (int)sm.clen[ka] : LB, lb_ = vb ? (int)sm.clen[kb] : LB;
+                int la_ = va ? (int)sm.clen[ka] : 0, lb_ = vb ? (int)sm.clen[kb] : 0;
+                const bool clean = kc + NWAP_CHUNK <= nclean;             // sorted part: the chunk's first word is its longest
+                const int lraw = clean ? (int)sm.clen[kc] : __reduce_max_sync(0xffffffffu, max(la_, lb_));
+                const int LB = min((lraw + NWAP_LBSTEP - 1) / NWAP_LBSTEP * NWAP_LBSTEP, MAXL);
+                if (!va) la_ = LB;
+                if (!vb) lb_ = LB;
                 const uint32_t off0 = va ? (uint32_t)sm.cols[ka] : 0xffffu;
                 const uint32_t off1 = vb ? (uint32_t)sm.cols[kb] : 0xffffu;
                 // column words (invalid lanes re-read the chunk's first column; their results are dropped)
@@ -991,7 +1002,7 @@ k_score_tiles(const nwap_tile_params p)
                 const nwap_lane_cols cA = nwap_make_lane_cols(off0, off1, la_, lb_, LB, sc);
                 const int lmin = __reduce_min_sync(0xffffffffu, min(la_, lb_));
                 const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
-                const bool fast = band_simple && (kc + NWAP_CHUNK <= ncols);
+                const bool fast = band_simple && clean;
                 if (WIDE && LB > QMAX) {
                     nwap_run_chunk_wide(LB, sm, sc, p.ids + ca * p.qpad, p.ids + cb * p.qpad, cA, fast, kNoHist, ls);
                     continue;
