@@ -86,7 +86,7 @@ size_t nwap_tile_smem_bytes(int family, int K)
     case 3: return sizeof(nwap_tile_smem_t<1>);
     case 4: {
         // the K x K table is the struct's last member: K = 0 asks for the largest alphabet
-        const size_t tab = K > 0 ? (((size_t)K * (size_t)K + 15u) & ~size_t(15)) : (size_t)NWAP_OV_MAXK * NWAP_OV_MAXK;
+        const size_t tab = K > 0 ? (((size_t)K * (size_t)K + 15u) & ~size_t(15)) : (size_t)NWAP_TAB_MAXK * NWAP_TAB_MAXK;
         return offsetof(nwap_tile_smem_t<2>, etab) + std::max<size_t>(16, tab);
     }
     case 5: case 7: return sizeof(nwap_tile_smem_t<0, NWAP_MAXLEN_WIDE>);
@@ -105,7 +105,7 @@ struct nwap_ctx {
     bool general = false;  // explicit similarity table installed
     bool sparse_ov = false; // ... and it is uniform + at most NWAP_MAX_OV overrides per symbol (packed kernel can run it)
     nwap_ov_row *d_ov = nullptr;
-    bool tab_ok = false;    // ... or it is dense but K <= 128: the packed kernel's table-driven flavour runs it
+    bool tab_ok = false;    // ... or any table over K <= 256 symbols: the packed kernel's table-driven flavour runs it
     int tab_max = 0;        // the table's maximum M (the table on the device holds M - sim)
     uint8_t *d_etab = nullptr;
     std::vector<uint8_t> h_lens;        // host copy for shard arithmetic
@@ -287,7 +287,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     if (variant == NWAP_VARIANT_AUTO)
         variant = tab_ok ? NWAP_VARIANT_PACKED_TAB : (fast_ok || wide_ok) ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
     if (variant == NWAP_VARIANT_PACKED_TAB && !tab_ok)
-        return fail(NWAP_EINVAL, "packed_tab kernel needs a dense similarity table with K <= %d and max word length <= %d", NWAP_OV_MAXK, NWAP_MAXLEN_FAST);
+        return fail(NWAP_EINVAL, "packed_tab kernel needs a similarity table (overrides) with K <= %d and max word length <= %d", NWAP_TAB_MAXK, NWAP_MAXLEN_FAST);
     if (variant == NWAP_VARIANT_PACKED_SYM && !sym_ok)
         return fail(NWAP_EINVAL, "packed_sym kernel needs a uniform scheme with match >= mismatch and max word length <= %d (have %d%s)",
                     NWAP_MAXLEN_FAST, c->qmax, c->general ? ", similarity overrides" : "");
@@ -503,7 +503,7 @@ int nwap_set_similarity(nwap_ctx *c, const int8_t *sim, int K)
     }
     // dense but small alphabet: E = M - sim for the packed kernel's table-driven flavour
     if (c->d_etab) { CK(cudaDeviceSynchronize()); dev_free(c->d_etab); c->d_etab = nullptr; }
-    c->tab_ok = K <= NWAP_OV_MAXK;       // (a sparse table can run either way; `auto` prefers the sparse-override cell)
+    c->tab_ok = K <= NWAP_TAB_MAXK;       // (a sparse table can run either way; `auto` prefers the sparse-override cell)
     std::vector<uint8_t> etab;
     if (c->tab_ok) {
         c->tab_max = mx;

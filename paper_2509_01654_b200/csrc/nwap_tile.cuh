@@ -160,6 +160,8 @@ __device__ __forceinline__ int nwap_meta_skew(const nwap_row_meta &m, int rr) { 
 // shared memory carve-up of k_score_tiles
 // ---------------------------------------------------------------------------
 #define NWAP_OV_MAXK 128               // largest alphabet the sparse-override table holds in shared memory
+#define NWAP_TAB_MAXK 256              // largest alphabet of the table-driven cell: K x K bytes of dynamic shared memory
+                                       // (64 KB at 256 symbols: one CTA per SM; two up to ~100 symbols)
 template <int MODE> struct nwap_sym_of { typedef nwap_sym2 type; };
 template <> struct nwap_sym_of<1> { typedef nwap_sym8 type; };
 
@@ -185,7 +187,7 @@ struct nwap_tile_smem_t {
     int next_chunk;
     // dense-table mode: K x K bytes of M - sim.  LAST member: the launch sizes the dynamic shared memory to the
     // alphabet actually used (nwap_tile_smem_bytes), so that tables of up to ~100 symbols leave room for two CTAs per SM
-    alignas(16) uint8_t etab[MODE == 2 ? NWAP_OV_MAXK * NWAP_OV_MAXK : 16];
+    alignas(16) uint8_t etab[MODE == 2 ? NWAP_TAB_MAXK * NWAP_TAB_MAXK : 16];
 };
 
 typedef nwap_tile_smem_t<0> nwap_tile_smem;

@@ -457,8 +457,9 @@ def test_sparse_override_schemes_on_the_packed_kernel():
 
 
 def test_dense_similarity_tables_on_the_packed_kernel():
-    """Dense override tables (every pair has its own value) with K <= 128 run on the packed kernel's table-driven
-    flavour: same bytes and statistics as the generic kernel and the oracle; K > 128 falls back to the generic one."""
+    """Dense override tables (every pair has its own value) run on the packed kernel's table-driven flavour for every
+    alphabet the uint8 word store admits (K <= 256; the K x K table is dynamic shared memory): same bytes and statistics
+    as the generic kernel and the oracle."""
     rng = np.random.default_rng(314)
     for trial, (K, q, n) in enumerate([(6, 8, 300), (40, 24, 2500), (128, 16, 1200), (17, 32, 700), (3, 1, 50), (40, 12, 5200)]):
         while True:
@@ -489,13 +490,25 @@ def test_dense_similarity_tables_on_the_packed_kernel():
     with NwapContext(ids, lens, nw.ScoringScheme(1, -1, -1)) as ctx:
         with pytest.raises(ValueError, match="packed_tab"):
             ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed_tab")
-    # K > 128: generic kernel
-    K, n, q = 200, 150, 6
+    # 128 < K <= 256: still the table-driven cell (one CTA per SM: the table takes up to 64 KB)
+    for K, n, q in ((200, 900, 6), (256, 700, 9)):
+        ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
+        ids[0, 0] = K - 1
+        lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
+        ov = {(a, b): int((a * 7 + b * 3) % 5 - 2) for a in range(K) for b in range(a, K)}
+        scheme = nw.ScoringScheme(1, -1, -2, overrides=ov)
+        ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, nw.num_edges(n), threads=4)
+        with NwapContext(ids, lens, scheme) as ctx:
+            for v in ("auto", "packed_tab", "simple"):
+                got, st = _score(ctx, 0, nw.num_edges(n), v)
+                assert np.array_equal(got, ref), (K, v)
+                assert st[:4] == (rsum, rmin, rmax, nw.num_edges(n))
+    # words over 32 symbols with an override scheme: the generic kernel
+    K, n, q = 12, 300, 40
     ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
-    ids[0, 0] = K - 1
     lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
-    ov = {(a, b): int((a * 7 + b * 3) % 5 - 2) for a in range(K) for b in range(a, K)}
-    scheme = nw.ScoringScheme(1, -1, -2, overrides=ov)
+    lens[0] = q
+    scheme = nw.ScoringScheme(1, -1, -1, overrides={(0, 1): 0, (2, 3): 1})
     ref, *_ = _oracle(ids, lens, scheme, 0, nw.num_edges(n))
     with NwapContext(ids, lens, scheme) as ctx:
         got, _ = _score(ctx, 0, nw.num_edges(n), "auto")
