@@ -46,8 +46,8 @@ extern "C" {
 #define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 DPX + 2 IMAD per packed cell */
 #define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 2 DPX + 1 IMAD + 1 IADD per packed cell; word length <= 64
                                  * (chunks longer than 24 symbols are scored block-wise, 16 columns at a time) */
-#define NWAP_VARIANT_PACKED_TAB 5 /* s16x2 DPX tile kernel with a K x K similarity table in shared memory (K <= 128):
-                                   * dense override tables; 2 byte loads per packed cell instead of compare + multiply */
+#define NWAP_VARIANT_PACKED_TAB 5 /* s16x2 DPX tile kernel with a K x K similarity table in shared memory (K <= 256):
+                                   * any override table; 2 byte loads per packed cell instead of compare + multiply */
 #define NWAP_VARIANT_PACKED_SYM 4 /* s16x2 DPX tile kernel, symmetric gap potential: 2 DPX + 1 IADD3 per packed cell
                                    * (needs match >= mismatch and no overrides) */
 
@@ -89,10 +89,11 @@ int nwap_create(nwap_ctx **ctx_out, int device,
 
 /* ScoringScheme.overrides (aligner.py:51-65, engine.py:113-116): install a
  * dense symmetric K x K similarity table (host int8, row-major).  Symbols >= K
- * are rejected.  With K <= 128 the packed tile kernel runs the table through its table-driven
- * flavour (NWAP_VARIANT_PACKED_TAB, what NWAP_VARIANT_AUTO picks); a table that is the uniform
- * scheme plus at most 3 overrides per symbol can also run as corrections of the compare-based
- * cell (NWAP_VARIANT_PACKED3); anything else goes to the generic one-thread-per-pair kernel. */
+ * are rejected.  The packed tile kernel runs the table through its table-driven flavour
+ * (NWAP_VARIANT_PACKED_TAB, what NWAP_VARIANT_AUTO picks; K <= 256, words of up to 32 symbols); a table
+ * that is the uniform scheme plus at most 2 overrides per symbol (K <= 128) can also run as corrections
+ * of the compare-based cell (NWAP_VARIANT_PACKED3); an override scheme with longer words goes to the
+ * generic one-thread-per-pair kernel. */
 int nwap_set_similarity(nwap_ctx *ctx, const int8_t *sim, int K);
 
 void nwap_destroy(nwap_ctx *ctx);
