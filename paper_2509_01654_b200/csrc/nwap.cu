@@ -189,7 +189,8 @@ int ensure_device_cache(int device, device_cache **out)
             for (int w = 0; w < 3; ++w) {
                 nwap_tile_kernel_t k = nwap_tile_kernel(f, w);
                 const size_t smem = nwap_tile_smem_bytes(f);
-                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                // the table flavour's launch adds its row-pair profiles (enqueue_score): allow it the whole SM
+                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, f == 4 ? 226 * 1024 : (int)smem));
                 int occ = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem));
                 dc.occ_tiles[f * 3 + w] = occ;
@@ -340,7 +341,14 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     else memset(&p.sparse, 0, sizeof p.sparse);
 
     int occ = std::max(1, c->occ_tiles[family * 3 + qclass]);
-    const size_t smem_bytes = nwap_tile_smem_bytes(family, tab ? c->K : 0);
+    p.tab2_lmax = 0;
+    size_t smem_bytes = nwap_tile_smem_bytes(family, tab ? c->K : 0);
+    if (tab) {
+        // second shape of the table cell (one load per packed cell): row-pair profiles behind the table, when they fit
+        static const bool no_tab2 = getenv("NWAP_NO_TAB2") && atoi(getenv("NWAP_NO_TAB2")) != 0;
+        const size_t prof = sizeof(uint32_t) * (size_t)NWAP_TAB2_PAIRS * (size_t)c->qmax * (size_t)c->K + sizeof(nwap_pair_meta) * NWAP_TAB2_PAIRS;
+        if (!no_tab2 && smem_bytes + prof <= (size_t)226 * 1024) { smem_bytes += prof; p.tab2_lmax = c->qmax; }
+    }
     if (tab) {          // the table-driven flavour's footprint depends on the alphabet: two CTAs per SM up to ~100 symbols
         int o = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, nwap_tile_kernel(family, qclass), NWAP_THREADS, smem_bytes));

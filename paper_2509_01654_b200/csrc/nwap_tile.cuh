@@ -140,6 +140,7 @@ struct nwap_tile_params {
     const nwap_ov_row *ov_table;   // sparse-override mode: (ov_K) rows on the device, else NULL
     int ov_K;                      // alphabet size K of the override / dense table
     const uint8_t *etab;           // dense-table mode (FLAVOR 3): K x K table of M - sim on the device, else NULL
+    int tab2_lmax;                 // FLAVOR 3: > 0 = the row-pair profiles fit shared memory (rows per profile), see nwap_chunk_rows_tab2
     nwap_sparse_out sparse;        // CMP instantiations only
 };
 
@@ -515,6 +516,112 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
 }
 
 
+// ---- table-driven cell, second shape (FLAVOR 3, round 2): ONE shared-memory load per packed cell -----------------
+// nwap_dp_row_tab packs two COLUMN words against one row word, so a packed cell needs two table entries of the same
+// table row, E[a_i][b0_j] and E[a_i][b1_j]: two LDS.U8, and the shared-memory pipe is the bound (9.3 TCUPS).  Here the
+// two halves of a register belong to two ROW words (rows 2p and 2p+1 of the band) against ONE column word per lane:
+// the packed cell needs E[a_i][b_j] | E[a'_i][b_j] << 16, which is ONE 32-bit load from the row pair's PROFILE
+//     W[p][i][b] = E[a_{2p,i}][b] | E[a_{2p+1,i}][b] << 16          (K words per matrix row, built per band)
+// at the lane's column symbol -- the cell is LDS.32, subtract, add, VIMNMX3, as many instructions as the uniform
+// scheme's.  The two row words differ in length: the pair runs min(la, la') matrix rows, captures the shorter word's
+// final cell, runs on to max(la, la') and captures the other (one loop, entered twice).  The boundary column is the
+// same for both halves (BIAS + i*u), so it is kept in a register and bumped per row.  The lane's two columns run as
+// two independent chains in the same loop.  Profiles: 8 pairs x lmax rows x K words -- 30 KB at 40 symbols and 24 rows; the
+// launch enables this shape when they fit (p.tab2_lmax > 0), and it serves the chunks the fast family serves (full,
+// every row live, at most three lengths); everything else runs nwap_run_chunk_tab.
+struct alignas(16) nwap_pair_meta {
+    int lmin, lmax;            // matrix rows of the shorter / longer word of the pair
+    uint32_t sel;              // halves of the SHORTER word: 0x0000ffff (row 2p) or 0xffff0000 (row 2p+1)
+    uint32_t ala2;             // row potentials: alpha*la(2p) | alpha*la(2p+1) << 16
+    int rowadj0, rowadj1;      // staged-byte bases of the two rows (nwap_row_meta::rowadj)
+    int pad0, pad1;
+};
+#define NWAP_TAB2_PAIRS (NWAP_R / 2)
+
+// Both of the lane's columns are scored in the same loop (two independent chains: the load -> subtract -> max3
+// latency of one hides behind the other; these builds run one CTA per SM, so registers are plentiful).
+template <int LB, int QW, class SM>
+__device__ __forceinline__ void nwap_chunk_rows_tab2(SM &sm, const nwap_scheme_consts &sc, const uint32_t (&w0)[QW],
+                                                     const uint32_t (&w1)[QW], const nwap_lane_cols &c, int K,
+                                                     int lmax_rows, const uint32_t *wprof, const nwap_pair_meta *pm,
+                                                     nwap_lane_stats &ls)
+{
+    uint32_t ca[LB], cb[LB];                                     // column symbols as byte offsets in a profile row
+#pragma unroll
+    for (int j = 0; j < LB; ++j) { ca[j] = 4u * nwap_byte_of(w0, j); cb[j] = 4u * nwap_byte_of(w1, j); }
+    const uint32_t kva = c.l0 == LB ? 0xffffffffu : 0u, k1a = c.l0 == LB - 1 ? 0xffffffffu : 0u;
+    const uint32_t kvb = c.l1 == LB ? 0xffffffffu : 0u, k1b = c.l1 == LB - 1 ? 0xffffffffu : 0u;
+    const uint32_t kposa = (uint32_t)(sc.beta * c.l0) * 65537u, kposb = (uint32_t)(sc.beta * c.l1) * 65537u;
+    uint32_t acc = 0, acc_hi = 0;
+    uint8_t *oa = sm.out + c.off0, *ob = sm.out + c.off1;
+#pragma unroll 1
+    for (int pr = 0; pr < NWAP_TAB2_PAIRS; ++pr) {
+        const nwap_pair_meta m = pm[pr];
+        const char *wr = reinterpret_cast<const char *>(wprof + (size_t)pr * lmax_rows * K);
+        uint32_t Pa[LB + 1], Pb[LB + 1];
+#pragma unroll
+        for (int j = 0; j <= LB; ++j) { Pa[j] = NWAP_BIAS2; Pb[j] = NWAP_BIAS2; }
+        uint32_t b0 = NWAP_BIAS2;                                // H'[i-1][0], the same for both halves and both columns
+        uint32_t va0 = 0, va1 = 0, vb0 = 0, vb1 = 0;
+        int rows = m.lmin;
+#pragma unroll 1
+        for (int ph = 0; ph < 2; ++ph) {
+#pragma unroll 1
+            for (; rows > 0; --rows) {
+                const uint32_t left0 = b0 + sc.u2;
+                uint32_t lefta = left0, leftb = left0;
+                uint32_t dwa = b0 - *reinterpret_cast<const uint32_t *>(wr + ca[0]);
+                uint32_t dwb = b0 - *reinterpret_cast<const uint32_t *>(wr + cb[0]);
+#pragma unroll
+                for (int j = 1; j <= LB; ++j) {
+                    uint32_t na = 0, nb_ = 0;
+                    if (j < LB) {
+                        na = Pa[j] - *reinterpret_cast<const uint32_t *>(wr + ca[j]);
+                        nb_ = Pb[j] - *reinterpret_cast<const uint32_t *>(wr + cb[j]);
+                    }
+                    const uint32_t cura = nwap_vimax3_s16x2(dwa, Pa[j] + sc.u2, lefta);
+                    const uint32_t curb = nwap_vimax3_s16x2(dwb, Pb[j] + sc.u2, leftb);
+                    Pa[j] = cura; lefta = cura; dwa = na;
+                    Pb[j] = curb; leftb = curb; dwb = nb_;
+                }
+                b0 = left0;
+                wr += 4 * K;
+            }
+            const uint32_t ta = (Pa[LB >= 2 ? LB - 1 : LB] & k1a) | (Pa[LB >= 3 ? LB - 2 : LB] & ~k1a);
+            const uint32_t tb = (Pb[LB >= 2 ? LB - 1 : LB] & k1b) | (Pb[LB >= 3 ? LB - 2 : LB] & ~k1b);
+            const uint32_t fa = (Pa[LB] & kva) | (ta & ~kva), fb = (Pb[LB] & kvb) | (tb & ~kvb);
+            if (ph == 0) { va0 = fa; vb0 = fb; } else { va1 = fa; vb1 = fb; }
+            rows = m.lmax - m.lmin;
+        }
+        // halves: score + BIAS of (row 2p, column) and (row 2p+1, column)
+        const uint32_t t_a = ((va0 & m.sel) | (va1 & ~m.sel)) + m.ala2 + kposa;
+        const uint32_t t_b = ((vb0 & m.sel) | (vb1 & ~m.sel)) + m.ala2 + kposb;
+        oa[m.rowadj0] = (uint8_t)t_a; oa[m.rowadj1] = (uint8_t)(t_a >> 16);
+        ob[m.rowadj0] = (uint8_t)t_b; ob[m.rowadj1] = (uint8_t)(t_b >> 16);
+        ls.mn2 = __vmins2(__vmins2(ls.mn2, t_a), t_b);
+        ls.mx2 = __vmaxs2(__vmaxs2(ls.mx2, t_a), t_b);
+        acc += t_a; acc_hi += t_a >> 16;
+        acc += t_b; acc_hi += t_b >> 16;
+    }
+    ls.sum += (long long)(acc - (acc_hi << 16)) + (long long)acc_hi - 4ll * NWAP_TAB2_PAIRS * (long long)NWAP_BIAS;
+    ls.count += 4 * NWAP_TAB2_PAIRS;
+}
+
+template <int QMAX, int QW, class SM>
+__device__ __forceinline__ void nwap_run_chunk_tab2(int LB, SM &sm, const nwap_scheme_consts &sc,
+                                                    const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
+                                                    const nwap_lane_cols &c, int K, int lmax_rows, const uint32_t *wprof,
+                                                    const nwap_pair_meta *pm, nwap_lane_stats &ls)
+{
+#define NWAP_CASE(n)                                                                                       \
+    case n:                                                                                                \
+        if (n <= QMAX) nwap_chunk_rows_tab2<(n <= QMAX ? n : 1), QW>(sm, sc, w0, w1, c, K, lmax_rows, wprof, pm, ls); \
+        break;
+    switch (LB) { NWAP_CASES_1_32 default: break; }
+#undef NWAP_CASE
+}
+
+
 // ---- the fast family, second shape (NWAP_FAST2=1) -------------------------------------------------------------
 // Serves chunks that are full, whose rows all cover the whole column window, and whose lanes span at most three
 // word lengths (mixmode <= 2) -- everything else goes through the compact per-row-dispatch family.  Compared with
@@ -809,7 +916,7 @@ __device__ __forceinline__ void nwap_sparse_row(SM &sm, const nwap_tile_params &
 // CMP: sparse-output mode (p.sparse): the flush stage scans the staged scores for kept edges; the dense store
 // happens only when p.out is non-NULL.
 template <int FLAVOR, int QMAX, bool OV, bool WIDE = false, bool CMP = false>
-__global__ void __launch_bounds__(NWAP_THREADS, ((OV || (FLAVOR == 3 && QMAX > 24)) ? 1 : NWAP_MINB))   // sparse-override builds run one CTA per SM (two lose: profiles/r02b_overrides.txt); the 32-wide table build needs > 96 registers
+__global__ void __launch_bounds__(NWAP_THREADS, ((OV || FLAVOR == 3) ? 1 : NWAP_MINB))   // sparse-override builds run one CTA per SM (two lose: profiles/r02b_overrides.txt); so do the table builds (their row-pair profiles fill the shared memory)
 k_score_tiles(const nwap_tile_params p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -829,6 +936,9 @@ k_score_tiles(const nwap_tile_params p)
     if (FLAVOR == 3) {
         for (int w = tid; w < p.ov_K * p.ov_K; w += NWAP_THREADS) sm.etab[w] = p.etab[w];
     }
+    // FLAVOR 3, second shape: row-pair profiles and pair records behind the table (dynamic shared memory, sized by the launch)
+    uint32_t *const tab2_prof = reinterpret_cast<uint32_t *>(sm.etab + (((size_t)p.ov_K * p.ov_K + 15u) & ~size_t(15)));
+    nwap_pair_meta *const tab2_pm = reinterpret_cast<nwap_pair_meta *>(tab2_prof + (size_t)NWAP_TAB2_PAIRS * p.tab2_lmax * p.ov_K);
     if (CMP && p.sparse.mode == 2)
         for (int b = tid; b < 256; b += NWAP_THREADS) sm.kbounds[b] = p.sparse.bounds[b];
     const nwap_sparse_consts skc = nwap_make_sparse_consts(p.sparse);
@@ -960,8 +1070,6 @@ k_score_tiles(const nwap_tile_params p)
                     }
                 }
             }
-            if (tid == 0) sm.next_chunk = 0;
-            __syncthreads();
             // simple band: all R rows present and neither end of the launch range clips one of them; every row then
             // covers the whole CLEAN part of the sorted columns (columns beyond the unit's last row: in a strip to the
             // right of the unit's rows that is every column).  Evaluated by every thread from launch scalars: no
@@ -969,6 +1077,35 @@ k_score_tiles(const nwap_tile_params p)
             const bool clip_first = p.r_first >= rb0 && p.r_first < rb0 + NWAP_R && p.c_start > strip_lo;
             const bool clip_last = p.r_last >= rb0 && p.r_last < rb0 + NWAP_R && p.c_end + 1 < strip_hi;
             const bool band_simple = rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax && !clip_first && !clip_last;
+            if (FLAVOR == 3 && p.tab2_lmax > 0 && band_simple) {
+                // row-pair profiles of the band (nwap_chunk_rows_tab2): one (pair, matrix row) per thread
+                const int lmx = p.tab2_lmax, K = p.ov_K;
+                for (int item = tid; item < NWAP_TAB2_PAIRS * lmx; item += NWAP_THREADS) {
+                    const int pr = item / lmx, i = item - pr * lmx;
+                    const int64_t r0 = rb0 + 2 * pr, r1 = r0 + 1;
+                    const int la0 = (int)p.lens[r0], la1 = (int)p.lens[r1];
+                    if (i >= max(la0, la1)) continue;
+                    const uint32_t a0 = i < la0 ? (uint32_t)p.ids[r0 * p.qpad + i] : 0u;
+                    const uint32_t a1 = i < la1 ? (uint32_t)p.ids[r1 * p.qpad + i] : 0u;
+                    const uint8_t *e0 = sm.etab + a0 * K, *e1 = sm.etab + a1 * K;
+                    uint32_t *w = tab2_prof + (size_t)item * K;
+                    for (int b = 0; b < K; ++b) w[b] = (uint32_t)e0[b] | ((uint32_t)e1[b] << 16);
+                }
+            }
+            if (tid == 0) sm.next_chunk = 0;
+            __syncthreads();
+            if (FLAVOR == 3 && p.tab2_lmax > 0 && band_simple) {
+                if (tid < NWAP_TAB2_PAIRS) {
+                    const nwap_row_meta &m0 = sm.meta[2 * tid], &m1 = sm.meta[2 * tid + 1];
+                    nwap_pair_meta pm;
+                    pm.lmin = min(m0.la, m1.la); pm.lmax = max(m0.la, m1.la);
+                    pm.sel = m0.la <= m1.la ? 0x0000ffffu : 0xffff0000u;
+                    pm.ala2 = (uint32_t)(sc.alpha * m0.la) + ((uint32_t)(sc.alpha * m1.la) << 16);
+                    pm.rowadj0 = m0.rowadj; pm.rowadj1 = m1.rowadj; pm.pad0 = pm.pad1 = 0;
+                    tab2_pm[tid] = pm;
+                }
+                __syncthreads();
+            }
 
             // ---- compute: warps pull chunks of 64 sorted columns, longest first ----
             const int ncols = sm.ncols, nclean = sm.nclean;
@@ -1010,7 +1147,10 @@ k_score_tiles(const nwap_tile_params p)
                     continue;
                 }
                 if (FLAVOR == 3) {
-                    nwap_run_chunk_tab<QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
+                    if (p.tab2_lmax > 0 && fast && mixmode <= 2)
+                        nwap_run_chunk_tab2<QMAX, QW>(LB, sm, sc, w0, w1, cA, p.ov_K, p.tab2_lmax, tab2_prof, tab2_pm, ls);
+                    else
+                        nwap_run_chunk_tab<QMAX, QW>(LB, sm, sc, w0, w1, cA, mixmode, fast, kNoHist, ls);
                     continue;
                 }
 #if NWAP_HOIST
