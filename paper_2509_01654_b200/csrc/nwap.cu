@@ -877,10 +877,11 @@ int nwap_hist_normalized(nwap_ctx *c, const int8_t *payload_dev, int64_t start, 
     if (c->qmax <= 100) {
         // joint (max length, score) bins: no per-edge division, 26 KB of shared memory at 24 symbols
         const size_t smem = sizeof(unsigned int) * (size_t)(256 + nwap_joint_mul(c->qmax)) * (size_t)(c->qmax + 1);
-        CK(cudaFuncSetAttribute(k_hist_norm_joint, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / (smem + 1024)));
-        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((runs + 511) / 512, (int64_t)c->sm_count * per_sm));
-        k_hist_norm_joint<<<(unsigned)blocks, 512, smem, st>>>(payload_dev, count, kp, (unsigned long long *)counts_dev, c->qmax);
+        CK(cudaFuncSetAttribute(k_hist_norm_joint_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int64_t wruns = (count + 15 + NWAP_HJ_RUN - 1) / NWAP_HJ_RUN;
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((wruns + 15) / 16, (int64_t)c->sm_count * per_sm));
+        k_hist_norm_joint_w<<<(unsigned)blocks, 512, smem, st>>>(payload_dev, count, kp, (unsigned long long *)counts_dev, c->qmax);
         g_launches++;
         CK(cudaGetLastError());
         return NWAP_OK;

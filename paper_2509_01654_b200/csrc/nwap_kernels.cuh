@@ -745,42 +745,75 @@ __device__ __forceinline__ uint32_t nwap_prmt(uint32_t a, uint32_t b, uint32_t s
     return d;
 }
 
+// Work distribution.  The L1 / shared pipe is this kernel's bound, and in its first version (one thread = 64 consecutive
+// edges, as in the compaction scan: 1.23 TB/s, ncu 99 %) most wavefronts were not the atomics: four LDG.128 that lie 64
+// bytes apart between neighbouring lanes (16 cache lines per warp instruction) plus seventeen LDG.32 of lengths with the
+// same stride: 64 + 272 wavefronts per 2048 edges against ~130 for the atomics.  Here a WARP owns 2048 consecutive
+// window bytes and lane l takes the 16-byte vectors 32k + l (k = 0..3):
+// every payload instruction covers 512 contiguous bytes (16 sectors), and the 16 lengths of a vector come from the two
+// aligned LDG.128 that hold them (16 sectors each across the warp).  Order does not matter
+// for a histogram.  (r, c) is recovered once per warp run; a run that crosses a row end or the ends of the slice
+// (one in ~300 at 600,000 words) takes the per-edge walk.
+#define NWAP_HJ_RUN 2048
 __global__ void __launch_bounds__(512)
-k_hist_norm_joint(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp, unsigned long long *counts,
-                  int mmax)
+k_hist_norm_joint_w(const int8_t *__restrict__ payload, int64_t count, const nwap_keep_params kp,
+                    unsigned long long *counts, int mmax)
 {
-    // bin address = m * JS + (score + 128), JS = 256 + jmul: with a stride of 256 words every m lands in the same bank
-    // for a given score and the warp's atomics serialise 3x (ncu: 130 M bank conflicts per 2 Gi edges, L1 at 99 %);
-    // 265 = 9 mod 32 spreads the ~25 hot (m, score) pairs over distinct banks
     extern __shared__ unsigned int jbins[];              // [(mmax + 1) * JS]
     const int jmul = nwap_joint_mul(mmax), JS = 256 + jmul;
     const int nb = (mmax + 1) * JS;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) jbins[b] = 0;
     __syncthreads();
+    const int lane = threadIdx.x & 31;
     const int64_t lead = (int64_t)(reinterpret_cast<uintptr_t>(payload) & 15u);
-    const int64_t runs = (lead + count + NWAP_CMP_PER_THREAD - 1) / NWAP_CMP_PER_THREAD;
-    for (int64_t run = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; run < runs; run += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k_first = run * NWAP_CMP_PER_THREAD - lead;
-        const int64_t kb = max(k_first, (int64_t)0);
-        if (kb >= count) continue;
-        int64_t r = nwap_row_of(kp.start + kb, kp.n);
-        int64_t c = nwap_col_of(kp.start + kb, kp.n, r);
-        int lr = (int)kp.lens[r];
-        if (k_first >= 0 && k_first + NWAP_CMP_PER_THREAD <= count && c + NWAP_CMP_PER_THREAD <= kp.n) {
-            uint32_t L[16];
-            nwap_load_lens64(kp.lens, c, L);
+    const int64_t runs = (lead + count + NWAP_HJ_RUN - 1) / NWAP_HJ_RUN;
+    // a warp owns a CONTIGUOUS range of runs, so the row is recovered once (fp64 estimate + fix-up: ~150 warp
+    // instructions, a fifth of the kernel when done per run) and then walked
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t rpw = (runs + nwarps - 1) / nwarps;
+    const int64_t run_lo = warp0 * rpw, run_hi = min(runs, run_lo + rpw);
+    int64_t r = -1, row0 = 0, row_end = 0;                       // row of the current edge: global edges [row0, row_end)
+    for (int64_t run = run_lo; run < run_hi; ++run) {
+        const int64_t k_run = run * NWAP_HJ_RUN - lead;          // edge offset of the run's window byte 0 (may be negative)
+        const int64_t kb = max(k_run, (int64_t)0);
+        const int64_t ke = min(k_run + (int64_t)NWAP_HJ_RUN, count) - 1;   // last live edge of the run
+        if (kb > ke) continue;
+        if (r < 0) {
+            r = nwap_row_of(kp.start + kb, kp.n);                // the same value in every lane
+            row0 = nwap_before_row(r, kp.n);
+            row_end = row0 + (kp.n - 1 - r);
+        }
+        while (kp.start + kb >= row_end) { ++r; row0 = row_end; row_end += kp.n - 1 - r; }
+        const bool whole = k_run >= 0 && k_run + NWAP_HJ_RUN <= count && kp.start + ke < row_end;
+        if (whole) {
+            const int lr = (int)kp.lens[r];
             const uint32_t lr4 = (uint32_t)lr * 0x01010101u;
+            const int64_t c_run = r + 1 + (kp.start + k_run - row0);     // column of the run's window byte 0
 #pragma unroll
-            for (int v = 0; v < NWAP_CMP_VEC; ++v) {
-                const uint4 q4 = *reinterpret_cast<const uint4 *>(payload + k_first + 16 * v);
+            for (int k = 0; k < NWAP_HJ_RUN / 512; ++k) {
+                const int off = 512 * k + 16 * lane;
+                const uint4 q4 = *reinterpret_cast<const uint4 *>(payload + k_run + off);
+                // lengths of columns c_run + off .. + 15: the two aligned 16-byte vectors that hold them (across the
+                // warp: 2 x 16 sectors instead of 5 x 16 with word loads), realigned by whole words (uniform: every
+                // lane of the run has the same misalignment) and then by bytes
+                const uintptr_t a = reinterpret_cast<uintptr_t>(kp.lens + c_run + off);
+                const uint4 *lp = reinterpret_cast<const uint4 *>(a & ~uintptr_t(15));
+                const uint4 v0 = __ldg(lp), v1 = __ldg(lp + 1);
+                const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(a & 3u);
+                uint32_t lw[5];
+                switch ((int)((a >> 2) & 3u)) {
+                case 0: lw[0] = v0.x; lw[1] = v0.y; lw[2] = v0.z; lw[3] = v0.w; lw[4] = v1.x; break;
+                case 1: lw[0] = v0.y; lw[1] = v0.z; lw[2] = v0.w; lw[3] = v1.x; lw[4] = v1.y; break;
+                case 2: lw[0] = v0.z; lw[1] = v0.w; lw[2] = v1.x; lw[3] = v1.y; lw[4] = v1.z; break;
+                default: lw[0] = v0.w; lw[1] = v1.x; lw[2] = v1.y; lw[3] = v1.z; lw[4] = v1.w; break;
+                }
                 const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t x = w[q] ^ 0x80808080u;                       // score + 128 per byte
-                    const uint32_t m4 = nwap_bytemax7(L[4 * v + q], lr4);
-                    const uint32_t s4 = m4 * (uint32_t)jmul;                     // per byte (mmax * jmul < 256: no carry): the swizzle term
-                    // key j = {x byte j, m4 byte j, 0, 0} (selector nibbles 8|k replicate the clear sign of a length
-                    // byte) = m * 256 + score + 128; adding byte j of s4 makes it m * JS + score + 128
+                    const uint32_t m4 = nwap_bytemax7(__byte_perm(lw[q], lw[q + 1], sel), lr4);
+                    const uint32_t s4 = m4 * (uint32_t)jmul;                     // swizzle term per byte (mmax * jmul < 256)
                     atomicAdd(&jbins[nwap_prmt(x, m4, 0xcc40u) + nwap_prmt(s4, 0u, 0x4440u)], 1u);
                     atomicAdd(&jbins[nwap_prmt(x, m4, 0xdd51u) + nwap_prmt(s4, 0u, 0x4441u)], 1u);
                     atomicAdd(&jbins[nwap_prmt(x, m4, 0xee62u) + nwap_prmt(s4, 0u, 0x4442u)], 1u);
@@ -789,26 +822,17 @@ k_hist_norm_joint(const int8_t *__restrict__ payload, int64_t count, const nwap_
             }
             continue;
         }
-#pragma unroll
-        for (int v = 0; v < NWAP_CMP_VEC; ++v) {
-            const int64_t k0 = k_first + 16 * v;
-            if (k0 + 16 <= 0 || k0 >= count) continue;
-            const uint4 q4 = nwap_cmp_load(payload, count, k0);
-            const uint32_t w[4] = {q4.x, q4.y, q4.z, q4.w};
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int64_t k = k0 + j;
-                if (k >= 0 && k < count) {
-                    const int m = max(lr, (int)kp.lens[c]);
-                    const uint32_t sb = ((w[j >> 2] >> (8 * (j & 3))) & 0xffu) ^ 0x80u;
-                    atomicAdd(&jbins[m * JS + (int)sb], 1u);
-                    if (++c == kp.n) { ++r; c = r + 1; lr = (int)kp.lens[min(r, kp.n - 1)]; }
-                }
-            }
+        // the run crosses a row end or an end of the slice: lane l walks edges kb + l, kb + l + 32, ...
+        for (int64_t k = kb + lane; k <= ke; k += 32) {
+            const int64_t rr = nwap_row_of(kp.start + k, kp.n);
+            const int64_t cc = nwap_col_of(kp.start + k, kp.n, rr);
+            const int m = max((int)kp.lens[rr], (int)kp.lens[cc]);
+            const int sb = (int)payload[k] + 128;
+            atomicAdd(&jbins[m * JS + sb], 1u);
         }
     }
     __syncthreads();
-    for (int b = JS + threadIdx.x; b < nb; b += blockDim.x) { // m = 0 never occurs (every word has >= 1 symbol)
+    for (int b = JS + threadIdx.x; b < nb; b += blockDim.x) {   // m = 0 never occurs (every word has >= 1 symbol)
         const unsigned int h = jbins[b];
         if (h) {
             const int m = b / JS, sb = b - m * JS;
