@@ -360,7 +360,6 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
                                                int want_hist, nwap_lane_stats &ls)
 {
     uint32_t nb[QMAX];
-#pragma unroll
     nwap_unpack_cols<FLAVOR, QMAX, QW>(w0, w1, nb);
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
     const bool deep = mixmode > 2;
@@ -503,7 +502,6 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
                                                  int want_hist, nwap_lane_stats &ls)
 {
     uint32_t nb[QMAX];
-#pragma unroll
     nwap_unpack_cols<FLAVOR, QMAX, QW>(w0, w1, nb);
     nwap_chunk_acc ca; ca.acc = 0; ca.acc_hi = 0; ca.rows_fast = 0;
 #define NWAP_CASE(n)                                                                                       \
