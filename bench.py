@@ -186,8 +186,10 @@ def cpu_reference_run(ids, lens, scheme, budget_s: float, threads: int):
 
 
 def kernel_source_digest() -> str:
+    """Digest of the DEVICE code (the kernel headers and the tile instantiation units; nwap.cu is host code)."""
     h = hashlib.blake2b(digest_size=8)
-    for f in sorted((ROOT / "paper_2509_01654_b200" / "csrc").glob("*.cu*")):
+    csrc = ROOT / "paper_2509_01654_b200" / "csrc"
+    for f in sorted(list(csrc.glob("*.cuh")) + list(csrc.glob("tiles_*.cu"))):
         h.update(f.read_bytes())
     return h.hexdigest()
 

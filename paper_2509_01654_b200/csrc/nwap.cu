@@ -5,6 +5,11 @@
 // for host destinations, equal-work shard bounds.  No CPU scoring path exists
 // here: every score is produced by a CUDA kernel or the call fails.
 #include <algorithm>
+#include <memory>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
+#include <chrono>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -418,9 +423,23 @@ int nwap_preflight(const uint8_t *lengths, int64_t n, int gap, int min_sim, int 
     return (int)q;
 }
 
+namespace {
+struct phase_timer {
+    bool on; std::chrono::steady_clock::time_point t0;
+    phase_timer() : on(getenv("NWAP_TIMING") != nullptr), t0(std::chrono::steady_clock::now()) {}
+    void mark(const char *what) {
+        if (!on) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[nwap timing] %-22s %8.1f us\n", what, std::chrono::duration<double, std::micro>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+}
+
 int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, int q_stride,
                 const uint8_t *lengths, int match, int mismatch, int gap)
 {
+    phase_timer pt;
     if (!ctx_out || !ids || !lengths) return fail(NWAP_EINVAL, "null argument");
     if (n < 2) return fail(NWAP_EINVAL, "need at least two words");
     if (device < 0 || device >= 64) return fail(NWAP_EINVAL, "device %d out of range", device);
@@ -428,18 +447,52 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
     int q = nwap_preflight(lengths, n, gap, std::min(match, mismatch), std::max(match, mismatch), nullptr, nullptr);
     if (q < 0) return q;
     if (q > q_stride) return fail(NWAP_EINVAL, "a word length (%d) exceeds q_stride (%d)", q, q_stride);
+    // one pass over the words: reject empty ones, repack the rows to qpad bytes (zero padded) and find the largest
+    // symbol.  16 bytes at a time with a per-length mask where the source row allows it (this pass and the repack
+    // were 3.3 of the 3.8 ms a context costs at 100,000 words, all of it inside the end-to-end step).
+    const int qpad_ = ((q + 15) / 16) * 16;
+    std::unique_ptr<uint8_t[]> packed(new uint8_t[(size_t)n * qpad_]);
     int maxsym = 0;
-    for (int64_t i = 0; i < n; ++i) {
-        const int len = lengths[i];
-        if (len < 1) return fail(NWAP_EINVAL, "word %lld is empty (length 0)", (long long)i);
-        for (int j = 0; j < len; ++j) maxsym = std::max<int>(maxsym, ids[i * q_stride + j]);
+    {
+        const int64_t total = n * (int64_t)q_stride;
+        int64_t i = 0;
+#if defined(__SSE2__)
+        alignas(16) uint8_t mask16[17][16];
+        for (int l = 0; l <= 16; ++l) for (int b = 0; b < 16; ++b) mask16[l][b] = b < l ? 0xff : 0x00;
+        __m128i mx = _mm_setzero_si128();
+        for (; i < n && i * (int64_t)q_stride + qpad_ <= total; ++i) {
+            const int len = lengths[i];
+            if (len < 1) return fail(NWAP_EINVAL, "word %lld is empty (length 0)", (long long)i);
+            const uint8_t *src = ids + i * q_stride;
+            uint8_t *dst = packed.get() + (size_t)i * qpad_;
+            for (int h = 0; h < qpad_; h += 16) {
+                const int lh = std::min(16, std::max(0, len - h));
+                const __m128i v = _mm_and_si128(_mm_loadu_si128(reinterpret_cast<const __m128i *>(src + h)),
+                                                _mm_load_si128(reinterpret_cast<const __m128i *>(mask16[lh])));
+                _mm_storeu_si128(reinterpret_cast<__m128i *>(dst + h), v);
+                mx = _mm_max_epu8(mx, v);
+            }
+        }
+        alignas(16) uint8_t mxb[16];
+        _mm_store_si128(reinterpret_cast<__m128i *>(mxb), mx);
+        for (int b = 0; b < 16; ++b) maxsym = std::max<int>(maxsym, mxb[b]);
+#endif
+        for (; i < n; ++i) {                                     // the last rows (and hosts without SSE2): bytewise
+            const int len = lengths[i];
+            if (len < 1) return fail(NWAP_EINVAL, "word %lld is empty (length 0)", (long long)i);
+            uint8_t *dst = packed.get() + (size_t)i * qpad_;
+            memset(dst, 0, qpad_);
+            for (int j = 0; j < len; ++j) { dst[j] = ids[i * q_stride + j]; maxsym = std::max<int>(maxsym, dst[j]); }
+        }
     }
+    pt.mark("validate");
     ON_DEVICE(device);
     device_cache *dc = nullptr;
     {
         const int rc0 = ensure_device_cache(device, &dc);
         if (rc0) return rc0;
     }
+    pt.mark("device cache");
     nwap_ctx *c = new nwap_ctx();
     c->sm_count = dc->sm_count;
     memcpy(c->occ_tiles, dc->occ_tiles, sizeof dc->occ_tiles);
@@ -453,32 +506,37 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
     for (int64_t r = 0; r < n; ++r)
         c->h_rowpref[r + 1] = c->h_rowpref[r] + (int64_t)lengths[r] * (c->h_lenprefix[n] - c->h_lenprefix[r + 1]);
 
-    // repack rows to qpad on the host, then one H2D copy
-    std::vector<uint8_t> packed((size_t)n * c->qpad, 0);
-    for (int64_t i = 0; i < n; ++i) memcpy(&packed[(size_t)i * c->qpad], ids + i * q_stride, lengths[i]);
+    pt.mark("prefix sums");
+    // (rows were repacked to qpad above) one H2D copy
+    const size_t packed_bytes = (size_t)n * c->qpad;
+    pt.mark("repack");
     const int64_t lens_pad = ((n + NWAP_C - 1) / NWAP_C) * NWAP_C + NWAP_C;
     int rc = NWAP_OK;
     auto guard = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess && rc == NWAP_OK) rc = fail(NWAP_ECUDA, "%s failed: %s", what, cudaGetErrorString(e));
     };
-    guard(dev_alloc(&c->d_ids, packed.size()), "alloc(ids)");
+    guard(dev_alloc(&c->d_ids, packed_bytes), "alloc(ids)");
     guard(dev_alloc(&c->d_lens, lens_pad), "alloc(lens)");
     guard(dev_alloc(&c->d_stats, sizeof(nwap_dev_stats)), "alloc(stats)");
     guard(dev_alloc(&c->d_counter, sizeof(unsigned long long)), "alloc(counter)");
     guard(dev_alloc(&c->d_total, sizeof(long long)), "alloc(total)");
+    pt.mark("allocs");
     if (rc == NWAP_OK) {
-        guard(cudaMemcpyAsync(c->d_ids, packed.data(), packed.size(), cudaMemcpyHostToDevice, 0), "H2D ids");
+        guard(cudaMemcpyAsync(c->d_ids, packed.get(), packed_bytes, cudaMemcpyHostToDevice, 0), "H2D ids");
         guard(cudaMemsetAsync(c->d_lens, 0, lens_pad, 0), "memset lens");
         guard(cudaMemcpyAsync(c->d_lens, lengths, n, cudaMemcpyHostToDevice, 0), "H2D lens");
     }
+    pt.mark("H2D enqueue");
     if (rc == NWAP_OK) {
         // uniform-scheme similarity table (engine.py:110-112) for the generic kernel
         std::vector<int8_t> sim((size_t)c->K * c->K, (int8_t)mismatch);
         for (int k = 0; k < c->K; ++k) sim[(size_t)k * c->K + k] = (int8_t)match;
         rc = build_sim_table(c, sim.data());
     }
+    pt.mark("sim table");
     // the store must be complete before kernels on other (non-blocking) streams read it
     if (rc == NWAP_OK) guard(cudaStreamSynchronize(0), "H2D word store");
+    pt.mark("sync");
     if (rc != NWAP_OK) { nwap_destroy(c); return rc; }
     *ctx_out = c;
     return NWAP_OK;
