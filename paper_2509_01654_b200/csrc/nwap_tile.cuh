@@ -147,7 +147,8 @@ struct nwap_tile_params {
 struct alignas(16) nwap_row_meta {
     // first 16 bytes: everything the fast row path needs
     int la;            // row word length, 0 = row not in this launch / no valid column in this strip
-    uint32_t symend;   // shared-window address one past the row's last staged symbol record (matrix-row loop bound)
+    uint32_t symend;   // NWAP_CARRY_LOOP: (uint32)(-8 * la), the matrix-row loop's counter (see nwap_chunk_rows_fast2); else the
+                       // shared-window address one past the row's last staged symbol record
     uint32_t ala2;     // (alpha * la) * 65537: the row potential, packed for both halves
     int rowadj;        // smem byte index of (column offset 0): rr*PITCH + skew - clo_off
     int clo_off;       // first valid column, relative to the strip
@@ -160,6 +161,9 @@ __device__ __forceinline__ int nwap_meta_skew(const nwap_row_meta &m, int rr) { 
 // ---------------------------------------------------------------------------
 // shared memory carve-up of k_score_tiles
 // ---------------------------------------------------------------------------
+#ifndef NWAP_CARRY_LOOP
+#define NWAP_CARRY_LOOP 1              // matrix-row loop of the fast2 family: pointer bump and loop test in ONE IADD3 (carry-out)
+#endif
 #define NWAP_OV_MAXK 128               // largest alphabet the sparse-override table holds in shared memory
 #define NWAP_TAB_MAXK 256              // largest alphabet of the table-driven cell: K x K bytes of dynamic shared memory
                                        // (64 KB at 256 symbols: one CTA per SM; two up to ~100 symbols)
@@ -173,6 +177,11 @@ struct nwap_tile_smem_t {
     alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
     typedef typename nwap_sym_of<MODE>::type sym_t;
     alignas(16) sym_t rowsym[NWAP_R][MAXLEN + 1];                // {a*65537, H'[i+1][0] (, override row)} per matrix row
+    // first staged record of row rr.  NWAP_CARRY_LOOP: the 8-byte records of a row END at slot MAXLEN (so that the
+    // matrix-row loop can count a negative offset up to zero against a warp-uniform base); override rows start at 0.
+    static constexpr bool END_ALIGNED = NWAP_CARRY_LOOP && MODE != 1;
+    __device__ __forceinline__ const sym_t *syms(int rr, int la) const { return rowsym[rr] + (END_ALIGNED ? MAXLEN - la : 0); }
+    __device__ __forceinline__ sym_t *syms(int rr, int la) { return rowsym[rr] + (END_ALIGNED ? MAXLEN - la : 0); }
     alignas(16) nwap_ov_part ov[MODE == 1 ? NWAP_OV_MAXK : 1];      // per-symbol partner table (sparse-override mode)
     alignas(16) nwap_row_meta meta[NWAP_R + 1];                     // one readable record past the band (row prefetch)
     uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
@@ -369,7 +378,7 @@ __device__ __forceinline__ void nwap_run_chunk(int LB, SM &sm, const nwap_scheme
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
         if (la == 0) continue;                       // uniform across the CTA
-        const typename SM::sym_t *sym = sm.rowsym[rr];
+        const typename SM::sym_t *sym = sm.syms(rr, la);
         uint32_t v = 0, vm1 = 0, vm2 = 0;
 #define NWAP_CASE(n)                                                                                       \
     case n:                                                                                                \
@@ -420,7 +429,7 @@ __device__ __forceinline__ void nwap_chunk_rows_tab(SM &sm, const nwap_scheme_co
         const int la = m.la;
         if (la == 0) continue;
         uint32_t v, vm1, vm2;
-        nwap_row_dp_tab<LB>(reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]), la, c0, c1, c.l0, c.l1, sc, sm.etab,
+        nwap_row_dp_tab<LB>(reinterpret_cast<const nwap_sym2 *>(sm.syms(rr, la)), la, c0, c1, c.l0, c.l1, sc, sm.etab,
                             v, vm1, vm2, deep);
         if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
         nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
@@ -476,7 +485,7 @@ __device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_cons
             const uint4 cur = nxt;
             nxt = *reinterpret_cast<const uint4 *>(&sm.meta[rr + 1 < NWAP_R ? rr + 1 : rr]);
             uint32_t v, vm1, vm2;
-            nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, (int)cur.x, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+            nwap_row_dp<LB, FLAVOR>(sm.syms(rr, (int)cur.x), sm.ov, (int)cur.x, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
             if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
             nwap_emit(sm, sm.meta[rr], cur.z, (int)cur.w, v, c, nwap_true(), 0, ls, ca);
         }
@@ -488,7 +497,7 @@ __device__ __forceinline__ void nwap_chunk_rows_h(SM &sm, const nwap_scheme_cons
         const int la = m.la;
         if (!FASTONLY && la == 0) continue;
         uint32_t v, vm1, vm2;
-        nwap_row_dp<LB, FLAVOR>(sm.rowsym[rr], sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
+        nwap_row_dp<LB, FLAVOR>(sm.syms(rr, la), sm.ov, la, nb, c.l0, c.l1, sc, v, vm1, vm2, deep);
         if (mixmode == 1 || mixmode == 2) v = nwap_merge3(v, vm1, vm2, c);
         if (FASTONLY) nwap_emit(sm, m, m.ala2, m.rowadj, v, c, nwap_true(), 0, ls, ca);
         else nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
@@ -661,6 +670,14 @@ __device__ __forceinline__ uint4 nwap_lds128(uint32_t addr)
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
+// cnt += STEP; returns the carry-out (ptxas: one IADD3 with a predicate destination that the loop branch uses)
+template <int STEP>
+__device__ __forceinline__ bool nwap_bump_carry(uint32_t &cnt)
+{
+    uint32_t c;
+    asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, 0, 0;" : "+r"(cnt), "=r"(c) : "n"(STEP));
+    return c != 0;
+}
 __device__ __forceinline__ void nwap_sts8(uint32_t addr, uint32_t v)
 {
     asm volatile("st.shared.u8 [%0], %1;" :: "r"(addr), "r"(v));
@@ -678,7 +695,7 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
     const uint32_t out_s = (uint32_t)__cvta_generic_to_shared(sm.out);
     const uint32_t o0 = out_s + c.off0, o1 = out_s + c.off1;
     const uint32_t kpos2 = c.kpos2;
-    uint32_t sym_s = (uint32_t)__cvta_generic_to_shared(&sm.rowsym[0][0]);
+    uint32_t sym_s = (uint32_t)__cvta_generic_to_shared(SM::END_ALIGNED ? sm.syms(0, 0) : &sm.rowsym[0][0]);
     uint32_t meta_s = (uint32_t)__cvta_generic_to_shared(&sm.meta[0]);
     constexpr uint32_t SYM_PITCH = sizeof(sm.rowsym[0]);
     constexpr uint32_t META_PITCH = sizeof(nwap_row_meta);
@@ -714,6 +731,45 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
                 nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
                 d0 = x.y;
             }
+        } else if (SM::END_ALIGNED && LB <= NWAP_F2_DUFF_MAXLB) {
+            // as below, counted by carry: ea = -8 * la runs up to zero in steps of 16
+#pragma unroll
+            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
+            d0 = NWAP_BIAS2;
+            uint32_t cnt = ea;
+            bool done;
+            if (cnt & 8u) { cnt -= 8u; goto second_row_c; }
+#pragma unroll 1
+            do {
+                {
+                    const uint2 x = nwap_lds64(sa + cnt);
+                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
+                    d0 = x.y;
+                }
+            second_row_c:
+                {
+                    const uint2 x = nwap_lds64(sa + cnt + 8u);
+                    done = nwap_bump_carry<16>(cnt);
+                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
+                    d0 = x.y;
+                }
+            } while (!done);
+        } else if (SM::END_ALIGNED) {
+            // the row's records end at sa (warp-uniform: a uniform register); the counter ea = -8 * la runs up to
+            // zero, and the carry-out of its increment IS the loop test: LDS.64 [cnt + base], IADD3 (carry), branch
+            // -- one instruction less per matrix row than pointer bump + compare + branch
+#pragma unroll
+            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;     // H'[0][j]
+            d0 = NWAP_BIAS2;
+            uint32_t cnt = ea;
+            bool done;
+#pragma unroll 1
+            do {                                                 // la >= 1 always
+                const uint2 x = nwap_lds64(sa + cnt);
+                done = nwap_bump_carry<8>(cnt);
+                nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
+                d0 = x.y;
+            } while (!done);
         } else if (LB <= NWAP_F2_DUFF_MAXLB) {
             // two matrix rows per loop trip (one pointer bump, test, branch and no boundary move per two rows); a
             // word of odd length enters at the second copy
@@ -813,7 +869,7 @@ __device__ NWAP_WIDE_ATTR void nwap_run_chunk_wide(int LB, SM &sm, const nwap_sc
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
         if (la == 0) continue;
-        const uint32_t v = nwap_dp_blocks(reinterpret_cast<const nwap_sym2 *>(sm.rowsym[rr]), la, b0, b1, nblk, c.l0, c.l1, sc, save);
+        const uint32_t v = nwap_dp_blocks(reinterpret_cast<const nwap_sym2 *>(sm.syms(rr, la)), la, b0, b1, nblk, c.l0, c.l1, sc, save);
         nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
     }
     nwap_close_chunk(ls, ca);
@@ -1041,7 +1097,8 @@ k_score_tiles(const nwap_tile_params p)
                         m.g0 = nwap_before_row(r, p.n) + (clo - r - 1) - p.start;
                         const int skew = (int)((reinterpret_cast<uintptr_t>(p.out) + (uintptr_t)m.g0) & 15u);
                         m.rowadj = tid * NWAP_PITCH + skew - m.clo_off;
-                        m.symend = (uint32_t)__cvta_generic_to_shared(&sm.rowsym[tid][m.la]);
+                        m.symend = smem_t::END_ALIGNED ? (uint32_t)(-8 * m.la)
+                                                   : (uint32_t)__cvta_generic_to_shared(&sm.rowsym[tid][m.la]);
                         m.ala2 = (uint32_t)(sc.alpha * m.la * 65537);
                         if (OV) {
                             const int gsum = nwap_stage_row_ov(p.ids + r * p.qpad, m.la, p.ov_table, p.ov_K, sc,
@@ -1063,7 +1120,7 @@ k_score_tiles(const nwap_tile_params p)
                     for (int e = 0; e < 4; ++e) {
                         const uint32_t a = (v >> (8 * e)) & 0xffu;
                         if (q4 * 4 + e < la_r)           // slot [la] belongs to the boundary record
-                            nwap_stage_sym(sm.rowsym[rr][q4 * 4 + e], a, sc, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
+                            nwap_stage_sym(sm.syms(rr, la_r)[q4 * 4 + e], a, sc, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
                                            sm.ov, p.ov_K);
                     }
                 }
