@@ -177,7 +177,12 @@ NWAP_HD uint32_t nwap_pack_negb_f(uint32_t b0, uint32_t b1)
 // update is in place and the loop over matrix rows needs no register moves and
 // no unrolling -- which keeps the per-length code small enough for the
 // instruction cache (32 length-specialised bodies live in one kernel).
-template <int LB, int FLAVOR>
+//
+// DOM: the row starts at the matrix border (column 0).  There the boundary value is dominated by the `up` term of
+// column 1 -- H'[i][0] = H'[i-1][0] + u <= H'[i-1][1] + u, because the left move is free (H'[i-1][1] >= H'[i-1][0],
+// and H'[0][1] = H'[0][0]) -- so cell (i, 1) is max(dw, up + u), left0 is not read, and the staged record only has
+// to carry d0 = H'[i-1][0]: no register move per matrix row.
+template <int LB, int FLAVOR, bool DOM = false>
 NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
                          uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc)
 {
@@ -204,7 +209,7 @@ NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
         uint32_t cur;
         // up + u: halves stay in [0, 2^15), so a plain 32-bit add/IMAD of u*65537 is a packed add
         const uint32_t upu = FLAVOR == 0 ? P[j] * sc.one + sc.u2 : P[j] + sc.u2;
-        cur = nwap_vimax3_s16x2(dw, upu, left);
+        cur = (DOM && j == 1) ? nwap_vmaxs2(dw, upu) : nwap_vimax3_s16x2(dw, upu, left);
         P[j] = cur;
         left = cur;
         dw = dw_next;
@@ -212,9 +217,9 @@ NWAP_HD void nwap_dp_row(uint32_t a2, const uint32_t *nb, uint32_t (&P)[LB + 1],
 }
 
 // All la matrix rows of one row word; returns P[] holding matrix row la.
-// row_sym2[i] = {a_i * 65537, H'[i+1][0]}: the packed symbol of matrix row i+1 and that
-// row's boundary value (BIAS2 + (i+1)*u2, the same for every word), fetched together.
-struct nwap_sym2 { uint32_t a2, left0; };
+// row_sym2[i] = {row code of a_i, H'[i][0]}: the packed symbol of matrix row i+1 and the boundary value of the row
+// ABOVE it (BIAS2 + i*u2, the same for every word: the diagonal term of column 1), fetched together.
+struct nwap_sym2 { uint32_t a2, d0; };
 
 // PEEL (FLAVOR 1 only): matrix row 1 is peeled.  Every H'[0][j] is BIAS, so its diagonal term is BIAS - e*D, and
 // its up term BIAS + u equals the row's boundary value H'[1][0] the left chain starts from, i.e. it is absorbed:
@@ -227,7 +232,7 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
     if (PEEL && FLAVOR == 1) {
         const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
         const nwap_sym2 x0 = *s++;
-        uint32_t left = x0.left0;
+        uint32_t left = x0.d0 + sc.u2;                      // H'[1][0]
         P[0] = NWAP_BIAS2;
 #pragma unroll
         for (int j = 1; j <= LB; ++j) {
@@ -235,18 +240,15 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
             left = nwap_vmaxs2(dw, left);
             P[j] = left;
         }
-        uint32_t d0 = x0.left0;
 #pragma unroll 1
         while (s != e) {
             const nwap_sym2 x = *s++;
-            nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
-            d0 = x.left0;
+            nwap_dp_row<LB, FLAVOR, true>(x.a2, nb, P, x.d0, 0u, sc);
         }
         return;
     }
 #pragma unroll
     for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;        // H'[0][j]
-    uint32_t d0 = NWAP_BIAS2;                               // H'[0][0]
     const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
     if (FLAVOR == 2) {
         const uint32_t d0c = NWAP_BIAS2 + sc.c2;            // H'[i-1][0] + C: every boundary cell is BIAS
@@ -259,9 +261,8 @@ NWAP_HD void nwap_dp_word(const nwap_sym2 *row_sym2, int la, const uint32_t *nb,
     }
 #pragma unroll 1
     do {                                                    // la >= 1 always
-        const nwap_sym2 x = *s++;                           // {symbol, boundary} in one 8-byte load
-        nwap_dp_row<LB, FLAVOR>(x.a2, nb, P, d0, x.left0, sc);
-        d0 = x.left0;
+        const nwap_sym2 x = *s++;                           // {symbol, boundary of the row above} in one 8-byte load
+        nwap_dp_row<LB, FLAVOR, true>(x.a2, nb, P, x.d0, 0u, sc);
     } while (s != e);
 }
 
@@ -406,16 +407,16 @@ inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatc
 // the compare + multiply; c0/c1 hold the lane's column symbols as byte offsets.
 template <int LB>
 NWAP_HD void nwap_dp_row_tab(uint32_t rowoff, const uint32_t *c0, const uint32_t *c1, uint32_t (&P)[LB + 1],
-                             uint32_t d0, uint32_t left0, const nwap_scheme_consts &sc, const uint8_t *etab)
+                             uint32_t d0, const nwap_scheme_consts &sc, const uint8_t *etab)
 {
     const uint8_t *row = etab + rowoff;
-    uint32_t left = left0;
+    uint32_t left = 0;                                      // column 1: the boundary is dominated (nwap_dp_row, DOM)
     uint32_t dw = d0 - ((uint32_t)row[c0[0]] | ((uint32_t)row[c1[0]] << 16));
 #pragma unroll
     for (int j = 1; j <= LB; ++j) {
         uint32_t dw_next = 0;
         if (j < LB) dw_next = P[j] - ((uint32_t)row[c0[j]] | ((uint32_t)row[c1[j]] << 16));
-        const uint32_t cur = nwap_vimax3_s16x2(dw, P[j] + sc.u2, left);
+        const uint32_t cur = j == 1 ? nwap_vmaxs2(dw, P[j] + sc.u2) : nwap_vimax3_s16x2(dw, P[j] + sc.u2, left);
         P[j] = cur;
         left = cur;
         dw = dw_next;
@@ -428,13 +429,11 @@ NWAP_HD void nwap_dp_word_tab(const nwap_sym2 *row_sym2, int la, const uint32_t 
 {
 #pragma unroll
     for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
-    uint32_t d0 = NWAP_BIAS2;
     const nwap_sym2 *s = row_sym2, *e = row_sym2 + la;
 #pragma unroll 1
     do {
         const nwap_sym2 x = *s++;
-        nwap_dp_row_tab<LB>(x.a2, c0, c1, P, d0, x.left0, sc, etab);
-        d0 = x.left0;
+        nwap_dp_row_tab<LB>(x.a2, c0, c1, P, x.d0, sc, etab);
     } while (s != e);
 }
 
@@ -480,7 +479,7 @@ NWAP_HD uint32_t nwap_dp_blocks(const nwap_sym2 *row_sym2, int la, const uint8_t
 #pragma unroll 1
         for (int i = 0; i < la; ++i) {
             const nwap_sym2 x = row_sym2[i];
-            const uint32_t left0 = blk == 0 ? x.left0 : save[i];   // H'[i+1][WB*blk]
+            const uint32_t left0 = blk == 0 ? x.d0 + sc.u2 : save[i]; // H'[i+1][WB*blk]
             nwap_dp_row<NWAP_WB, 1>(x.a2, nb, P, d0, left0, sc);
             d0 = left0;
             save[i] = P[NWAP_WB];                                  // H'[i+1][WB*(blk+1)] for the next block

@@ -710,12 +710,11 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
         uint32_t P[LB + 1];
         uint32_t sa = sym_s;
         sym_s += SYM_PITCH;
-        uint32_t d0;
         if (PEEL) {
             // matrix row 1 (see nwap_dp_word<.., PEEL>): H'[1][j] = max(BIAS - e_j*D, H'[1][j-1])
             const uint2 x0 = nwap_lds64(sa);
             sa += 8u;
-            uint32_t left = x0.y;
+            uint32_t left = x0.y + sc.u2;                        // H'[1][0]
             P[0] = NWAP_BIAS2;
 #pragma unroll
             for (int j = 1; j <= LB; ++j) {
@@ -723,19 +722,16 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
                 left = nwap_vmaxs2(dw, left);
                 P[j] = left;
             }
-            d0 = x0.y;
 #pragma unroll 1
             while (sa != ea) {
                 const uint2 x = nwap_lds64(sa);
                 sa += 8u;
-                nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
-                d0 = x.y;
+                nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
             }
         } else if (SM::END_ALIGNED && LB <= NWAP_F2_DUFF_MAXLB) {
             // as below, counted by carry: ea = -8 * la runs up to zero in steps of 16
 #pragma unroll
             for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
-            d0 = NWAP_BIAS2;
             uint32_t cnt = ea;
             bool done;
             if (cnt & 8u) { cnt -= 8u; goto second_row_c; }
@@ -743,15 +739,13 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
             do {
                 {
                     const uint2 x = nwap_lds64(sa + cnt);
-                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
-                    d0 = x.y;
+                    nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
                 }
             second_row_c:
                 {
                     const uint2 x = nwap_lds64(sa + cnt + 8u);
                     done = nwap_bump_carry<16>(cnt);
-                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
-                    d0 = x.y;
+                    nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
                 }
             } while (!done);
         } else if (SM::END_ALIGNED) {
@@ -760,48 +754,41 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
             // -- one instruction less per matrix row than pointer bump + compare + branch
 #pragma unroll
             for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;     // H'[0][j]
-            d0 = NWAP_BIAS2;
             uint32_t cnt = ea;
             bool done;
 #pragma unroll 1
             do {                                                 // la >= 1 always
                 const uint2 x = nwap_lds64(sa + cnt);
                 done = nwap_bump_carry<8>(cnt);
-                nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
-                d0 = x.y;
+                nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
             } while (!done);
         } else if (LB <= NWAP_F2_DUFF_MAXLB) {
             // two matrix rows per loop trip (one pointer bump, test, branch and no boundary move per two rows); a
             // word of odd length enters at the second copy
 #pragma unroll
             for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
-            d0 = NWAP_BIAS2;
             if ((ea - sa) & 8u) { sa -= 8u; goto second_row; }
 #pragma unroll 1
             do {
                 {
                     const uint2 x = nwap_lds64(sa);
-                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
-                    d0 = x.y;
+                    nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
                 }
             second_row:
                 {
                     const uint2 x = nwap_lds64(sa + 8u);
-                    nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
-                    d0 = x.y;
+                    nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
                 }
                 sa += 16u;
             } while (sa != ea);
         } else {
 #pragma unroll
             for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;     // H'[0][j]
-            d0 = NWAP_BIAS2;
 #pragma unroll 1
             do {                                                 // la >= 1 always
                 const uint2 x = nwap_lds64(sa);
                 sa += 8u;
-                nwap_dp_row<LB, FLAVOR>(x.x, nb, P, d0, x.y, sc);
-                d0 = x.y;
+                nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
             } while (sa != ea);
         }
         const uint32_t v = nwap_merge3(P[LB], P[LB >= 2 ? LB - 1 : LB], P[LB >= 3 ? LB - 2 : LB], c);
@@ -835,9 +822,9 @@ __device__ __forceinline__ void nwap_run_chunk_fast2(int LB, SM &sm, const nwap_
 // hoisting the length dispatch out of the row loop, one symbol stream per band, dual-chain
 // chunks (4 columns per lane), a cold code family for chunks spanning >= 3 lengths.
 
-__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, const nwap_scheme_consts &sc, uint32_t left0, const nwap_ov_part *, int)
+__device__ __forceinline__ void nwap_stage_sym(nwap_sym2 &x, uint32_t a, const nwap_scheme_consts &sc, uint32_t d0, const nwap_ov_part *, int)
 {
-    x.a2 = nwap_row_code(a, sc); x.left0 = left0;
+    x.a2 = nwap_row_code(a, sc); x.d0 = d0;
 }
 __device__ __forceinline__ void nwap_stage_sym(nwap_sym8 &, uint32_t, const nwap_scheme_consts &, uint32_t, const nwap_ov_part *, int)
 {
@@ -1120,7 +1107,7 @@ k_score_tiles(const nwap_tile_params p)
                     for (int e = 0; e < 4; ++e) {
                         const uint32_t a = (v >> (8 * e)) & 0xffu;
                         if (q4 * 4 + e < la_r)           // slot [la] belongs to the boundary record
-                            nwap_stage_sym(sm.syms(rr, la_r)[q4 * 4 + e], a, sc, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e + 1) * sc.u2,
+                            nwap_stage_sym(sm.syms(rr, la_r)[q4 * 4 + e], a, sc, NWAP_BIAS2 + (uint32_t)(q4 * 4 + e) * sc.u2,
                                            sm.ov, p.ov_K);
                     }
                 }

@@ -13,7 +13,7 @@ static uint32_t run_pair(const uint8_t *a, int la, const uint8_t *b0, int lb0,
     nwap_sym2 row2[256];
     for (int i = 0; i < la; ++i) {
         row2[i].a2 = nwap_row_code(a[i], sc);
-        row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+        row2[i].d0 = NWAP_BIAS2 + (uint32_t)i * sc.u2;
 
     }
     uint32_t nb[LB];
@@ -64,7 +64,7 @@ static uint32_t run_pair_tab(const uint8_t *a, int la, const uint8_t *b0, int lb
     nwap_sym2 row2[256];
     for (int i = 0; i < la; ++i) {
         row2[i].a2 = (uint32_t)a[i] * (uint32_t)K;
-        row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+        row2[i].d0 = NWAP_BIAS2 + (uint32_t)i * sc.u2;
     }
     uint32_t c0[LB], c1[LB];
     for (int j = 0; j < LB; ++j) { c0[j] = j < lb0 ? b0[j] : 0u; c1[j] = j < lb1 ? b1[j] : 0u; }
@@ -136,7 +136,7 @@ int emul_pair_scores_wide(const uint8_t *a, int la, const uint8_t *b0, int lb0, 
     nwap_sym2 row2[NWAP_MAXLEN_WIDE + 1];
     for (int i = 0; i < la; ++i) {
         row2[i].a2 = nwap_row_code(a[i], sc);
-        row2[i].left0 = NWAP_BIAS2 + (uint32_t)(i + 1) * sc.u2;
+        row2[i].d0 = NWAP_BIAS2 + (uint32_t)i * sc.u2;
     }
     uint8_t p0[NWAP_MAXLEN_WIDE + NWAP_WB] = {0}, p1[NWAP_MAXLEN_WIDE + NWAP_WB] = {0};
     memcpy(p0, b0, lb0);
