@@ -147,8 +147,7 @@ struct nwap_tile_params {
 struct alignas(16) nwap_row_meta {
     // first 16 bytes: everything the fast row path needs
     int la;            // row word length, 0 = row not in this launch / no valid column in this strip
-    uint32_t symend;   // NWAP_CARRY_LOOP: (uint32)(-8 * la), the matrix-row loop's counter (see nwap_chunk_rows_fast2); else the
-                       // shared-window address one past the row's last staged symbol record
+    uint32_t symend;   // (uint32)(-8 * la): the matrix-row loop's counter, which runs up to zero (nwap_chunk_rows_fast2)
     uint32_t ala2;     // (alpha * la) * 65537: the row potential, packed for both halves
     int rowadj;        // smem byte index of (column offset 0): rr*PITCH + skew - clo_off
     int clo_off;       // first valid column, relative to the strip
@@ -161,9 +160,6 @@ __device__ __forceinline__ int nwap_meta_skew(const nwap_row_meta &m, int rr) { 
 // ---------------------------------------------------------------------------
 // shared memory carve-up of k_score_tiles
 // ---------------------------------------------------------------------------
-#ifndef NWAP_CARRY_LOOP
-#define NWAP_CARRY_LOOP 1              // matrix-row loop of the fast2 family: pointer bump and loop test in ONE IADD3 (carry-out)
-#endif
 #define NWAP_OV_MAXK 128               // largest alphabet the sparse-override table holds in shared memory
 #define NWAP_TAB_MAXK 256              // largest alphabet of the table-driven cell: K x K bytes of dynamic shared memory
                                        // (64 KB at 256 symbols: one CTA per SM; two up to ~100 symbols)
@@ -177,9 +173,9 @@ struct nwap_tile_smem_t {
     alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
     typedef typename nwap_sym_of<MODE>::type sym_t;
     alignas(16) sym_t rowsym[NWAP_R][MAXLEN + 1];                // {a*65537, H'[i+1][0] (, override row)} per matrix row
-    // first staged record of row rr.  NWAP_CARRY_LOOP: the 8-byte records of a row END at slot MAXLEN (so that the
-    // matrix-row loop can count a negative offset up to zero against a warp-uniform base); override rows start at 0.
-    static constexpr bool END_ALIGNED = NWAP_CARRY_LOOP && MODE != 1;
+    // first staged record of row rr.  The 8-byte records of a row END at slot MAXLEN (so that the matrix-row loop of
+    // the fast2 family can count a negative offset up to zero against a warp-uniform base); override rows start at 0.
+    static constexpr bool END_ALIGNED = MODE != 1;
     __device__ __forceinline__ const sym_t *syms(int rr, int la) const { return rowsym[rr] + (END_ALIGNED ? MAXLEN - la : 0); }
     __device__ __forceinline__ sym_t *syms(int rr, int la) { return rowsym[rr] + (END_ALIGNED ? MAXLEN - la : 0); }
     alignas(16) nwap_ov_part ov[MODE == 1 ? NWAP_OV_MAXK : 1];      // per-symbol partner table (sparse-override mode)
@@ -637,15 +633,15 @@ __device__ __forceinline__ void nwap_run_chunk_tab2(int LB, SM &sm, const nwap_s
 //   * the column codes are unpacked inside the length body (LB of them, not QMAX: three PRMT per two columns);
 //   * shared memory is addressed through 32-bit shared-window addresses, rows and metadata walked by pointer
 //     (meta[] has one readable record past the band: the next row's record is fetched a row ahead);
-//   * bodies up to NWAP_F2_DUFF_MAXLB run two matrix rows per loop trip (6 control instructions per two rows
-//     instead of 5 per row; beyond LB 8 the doubled body loses to instruction-cache misses);
-//   * NWAP_F2_PEEL_MAXLB > 0 peels the first matrix row of short bodies instead (nwap_dp_word<.., PEEL>; +0.8 % at
-//     LB <= 8, not additive with the two-row loop: off).  A/B record: profiles/r02a_ab_fast2.txt.
+//   * the matrix-row loop is counted by carry and carries no border column: three control instructions per matrix
+//     row (LDS.64, IADD3, branch);
+//   * bodies up to NWAP_F2_DUFF_MAXLB run two matrix rows per loop trip (four control instructions per two rows;
+//     beyond LB 8 the doubled body loses to instruction-cache misses).
+// A peeled first matrix row (three instructions per cell, no initialisation of the rolling row) executes 2 * LB
+// fewer instructions per row word and is still SLOWER (-1.8 % for LB <= 8 ... -3.7 % for all bodies): code size.
+// A/B records: profiles/r02a_ab_fast2.txt, profiles/r02c_ab_rowloop.txt.
 #ifndef NWAP_FAST2
 #define NWAP_FAST2 1
-#endif
-#ifndef NWAP_F2_PEEL_MAXLB
-#define NWAP_F2_PEEL_MAXLB 0
 #endif
 #ifndef NWAP_F2_DUFF_MAXLB
 #define NWAP_F2_DUFF_MAXLB 8
@@ -688,108 +684,60 @@ __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_
                                                       const uint32_t (&w1)[QW], const nwap_lane_cols &c,
                                                       nwap_lane_stats &ls)
 {
-    constexpr bool PEEL = LB <= NWAP_F2_PEEL_MAXLB && FLAVOR == 1;
     uint32_t nb[LB];
     nwap_unpack_cols<FLAVOR, LB, QW>(w0, w1, nb);
     uint32_t acc = 0, acc_hi = 0;
     const uint32_t out_s = (uint32_t)__cvta_generic_to_shared(sm.out);
     const uint32_t o0 = out_s + c.off0, o1 = out_s + c.off1;
-    const uint32_t kpos2 = c.kpos2;
-    uint32_t sym_s = (uint32_t)__cvta_generic_to_shared(SM::END_ALIGNED ? sm.syms(0, 0) : &sm.rowsym[0][0]);
+    // through a shuffle: opaque to ptxas, which otherwise re-derives beta * lengths with a constant load per row word
+    const uint32_t kpos2 = __shfl_sync(0xffffffffu, c.kpos2, (int)(threadIdx.x & 31u));
+    static_assert(SM::END_ALIGNED, "fast2 serves the uniform-scheme builds");
+    uint32_t sym_s = (uint32_t)__cvta_generic_to_shared(sm.syms(0, 0));       // END of row 0's records
     uint32_t meta_s = (uint32_t)__cvta_generic_to_shared(&sm.meta[0]);
     constexpr uint32_t SYM_PITCH = sizeof(sm.rowsym[0]);
     constexpr uint32_t META_PITCH = sizeof(nwap_row_meta);
     uint4 nxt = nwap_lds128(meta_s);
 #pragma unroll 1
     for (int rr = 0; rr < NWAP_R; ++rr) {
-        // the whole 16-byte record {la, symend, ala2, rowadj} is fetched a row ahead
-        const uint32_t ea = nxt.y;
+        // the whole 16-byte record {la, -8 * la, ala2, rowadj} is fetched a row ahead
+        const uint32_t nxt_cnt = nxt.y;
         const uint2 cur = make_uint2(nxt.z, nxt.w);
         meta_s += META_PITCH;
         nxt = nwap_lds128(meta_s);                               // meta[] has one readable record past the band
         uint32_t P[LB + 1];
-        uint32_t sa = sym_s;
+        const uint32_t sa = sym_s;
         sym_s += SYM_PITCH;
-        if (PEEL) {
-            // matrix row 1 (see nwap_dp_word<.., PEEL>): H'[1][j] = max(BIAS - e_j*D, H'[1][j-1])
-            const uint2 x0 = nwap_lds64(sa);
-            sa += 8u;
-            uint32_t left = x0.y + sc.u2;                        // H'[1][0]
-            P[0] = NWAP_BIAS2;
+        // The row's records END at sa (warp-uniform: a uniform register); the counter -8 * la runs up to zero and the
+        // carry-out of its increment IS the loop test: LDS.64 [cnt + base], IADD3 (carry), branch -- three control
+        // instructions per matrix row (pointer bump + compare + move + branch + load were five).  The border column
+        // needs no register: see nwap_dp_row<.., DOM>.
 #pragma unroll
-            for (int j = 1; j <= LB; ++j) {
-                const uint32_t dw = nwap_viaddmin_u16x2(x0.x, nb[j - 1], 0x00010001u) * sc.neg_delta + NWAP_BIAS2;
-                left = nwap_vmaxs2(dw, left);
-                P[j] = left;
-            }
-#pragma unroll 1
-            while (sa != ea) {
-                const uint2 x = nwap_lds64(sa);
-                sa += 8u;
-                nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
-            }
-        } else if (SM::END_ALIGNED && LB <= NWAP_F2_DUFF_MAXLB) {
-            // as below, counted by carry: ea = -8 * la runs up to zero in steps of 16
-#pragma unroll
-            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
-            uint32_t cnt = ea;
-            bool done;
-            if (cnt & 8u) { cnt -= 8u; goto second_row_c; }
+        for (int j = 1; j <= LB; ++j) P[j] = NWAP_BIAS2;         // H'[0][j]
+        uint32_t cnt = nxt_cnt;
+        bool done;
+        if (LB <= NWAP_F2_DUFF_MAXLB) {
+            // two matrix rows per loop trip; a word of odd length enters at the second copy
+            if (cnt & 8u) { cnt -= 8u; goto second_row; }
 #pragma unroll 1
             do {
                 {
                     const uint2 x = nwap_lds64(sa + cnt);
                     nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
                 }
-            second_row_c:
+            second_row:
                 {
                     const uint2 x = nwap_lds64(sa + cnt + 8u);
                     done = nwap_bump_carry<16>(cnt);
                     nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
                 }
             } while (!done);
-        } else if (SM::END_ALIGNED) {
-            // the row's records end at sa (warp-uniform: a uniform register); the counter ea = -8 * la runs up to
-            // zero, and the carry-out of its increment IS the loop test: LDS.64 [cnt + base], IADD3 (carry), branch
-            // -- one instruction less per matrix row than pointer bump + compare + branch
-#pragma unroll
-            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;     // H'[0][j]
-            uint32_t cnt = ea;
-            bool done;
+        } else {
 #pragma unroll 1
             do {                                                 // la >= 1 always
                 const uint2 x = nwap_lds64(sa + cnt);
                 done = nwap_bump_carry<8>(cnt);
                 nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
             } while (!done);
-        } else if (LB <= NWAP_F2_DUFF_MAXLB) {
-            // two matrix rows per loop trip (one pointer bump, test, branch and no boundary move per two rows); a
-            // word of odd length enters at the second copy
-#pragma unroll
-            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;
-            if ((ea - sa) & 8u) { sa -= 8u; goto second_row; }
-#pragma unroll 1
-            do {
-                {
-                    const uint2 x = nwap_lds64(sa);
-                    nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
-                }
-            second_row:
-                {
-                    const uint2 x = nwap_lds64(sa + 8u);
-                    nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
-                }
-                sa += 16u;
-            } while (sa != ea);
-        } else {
-#pragma unroll
-            for (int j = 0; j <= LB; ++j) P[j] = NWAP_BIAS2;     // H'[0][j]
-#pragma unroll 1
-            do {                                                 // la >= 1 always
-                const uint2 x = nwap_lds64(sa);
-                sa += 8u;
-                nwap_dp_row<LB, FLAVOR, true>(x.x, nb, P, x.y, 0u, sc);
-            } while (sa != ea);
         }
         const uint32_t v = nwap_merge3(P[LB], P[LB >= 2 ? LB - 1 : LB], P[LB >= 3 ? LB - 2 : LB], c);
         const uint32_t t = v + cur.x + kpos2;                    // halves: score + BIAS
@@ -1084,8 +1032,7 @@ k_score_tiles(const nwap_tile_params p)
                         m.g0 = nwap_before_row(r, p.n) + (clo - r - 1) - p.start;
                         const int skew = (int)((reinterpret_cast<uintptr_t>(p.out) + (uintptr_t)m.g0) & 15u);
                         m.rowadj = tid * NWAP_PITCH + skew - m.clo_off;
-                        m.symend = smem_t::END_ALIGNED ? (uint32_t)(-8 * m.la)
-                                                   : (uint32_t)__cvta_generic_to_shared(&sm.rowsym[tid][m.la]);
+                        m.symend = (uint32_t)(-8 * m.la);
                         m.ala2 = (uint32_t)(sc.alpha * m.la * 65537);
                         if (OV) {
                             const int gsum = nwap_stage_row_ov(p.ids + r * p.qpad, m.la, p.ov_table, p.ov_K, sc,
