@@ -351,7 +351,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     if (tab) {
         // second shape of the table cell (one load per packed cell): row-pair profiles behind the table, when they fit
         static const bool no_tab2 = getenv("NWAP_NO_TAB2") && atoi(getenv("NWAP_NO_TAB2")) != 0;
-        const size_t prof = sizeof(uint32_t) * (size_t)NWAP_TAB2_PAIRS * (size_t)c->qmax * (size_t)c->K + sizeof(nwap_pair_meta) * NWAP_TAB2_PAIRS;
+        const size_t prof = nwap_tab2_prof_bytes(c->qmax, c->K) + sizeof(nwap_pair_meta) * NWAP_TAB2_PAIRS;
         if (!no_tab2 && smem_bytes + prof <= (size_t)226 * 1024) { smem_bytes += prof; p.tab2_lmax = c->qmax; }
     }
     if (tab) {          // the table-driven flavour's footprint depends on the alphabet: two CTAs per SM up to ~100 symbols
@@ -362,12 +362,13 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     const int64_t slots = (int64_t)c->sm_count * occ;
     // bands per group: as large as possible (amortises the per-unit sort) while
     // leaving >= 24 units per resident CTA for dynamic balance.
-    const int bands_per_strip = NWAP_C / NWAP_R;
+    const int cw = tab ? NWAP_TAB_CW : NWAP_C;              // strip width of the build (nwap_tile_smem_t<..>::C)
+    const int bands_per_strip = cw / NWAP_R;
     int gb = 16;
     nwap_unit_space us;
     int64_t ubeg = 0, ucount = 0;
     for (;; gb >>= 1) {
-        us.n = c->n; us.S = (c->n + NWAP_C - 1) / NWAP_C; us.gb = gb; us.gpk = bands_per_strip / gb;
+        us.n = c->n; us.S = (c->n + cw - 1) / cw; us.gb = gb; us.gpk = bands_per_strip / gb;
         const int64_t rows_per_group = (int64_t)gb * NWAP_R;
         const int64_t g0 = p.r_first / rows_per_group, g1 = p.r_last / rows_per_group;
         ubeg = nwap_units_before_group(us, g0);

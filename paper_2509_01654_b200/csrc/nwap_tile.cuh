@@ -34,7 +34,6 @@
 #define NWAP_UNITS_PER_SLOT 48
 #endif
 #define NWAP_WARPS (NWAP_THREADS / 32)
-#define NWAP_PITCH (NWAP_C + 16)         // bytes per staged output row (multiple of 16)
 #define NWAP_MAXLEN_FAST 32              // register-resident row limit
 #ifndef NWAP_WIDE_FROM
 #define NWAP_WIDE_FROM 32                // vocabularies whose longest word exceeds this run the wide build
@@ -155,7 +154,8 @@ struct alignas(16) nwap_row_meta {
     int64_t g0;        // out-relative byte offset of the segment
 };
 // (global address of the row's segment) & 15: the staged row is skewed so shared and global addresses agree mod 16
-__device__ __forceinline__ int nwap_meta_skew(const nwap_row_meta &m, int rr) { return m.rowadj - rr * NWAP_PITCH + m.clo_off; }
+template <int PITCH>
+__device__ __forceinline__ int nwap_meta_skew(const nwap_row_meta &m, int rr) { return m.rowadj - rr * PITCH + m.clo_off; }
 
 // ---------------------------------------------------------------------------
 // shared memory carve-up of k_score_tiles
@@ -168,9 +168,18 @@ template <> struct nwap_sym_of<1> { typedef nwap_sym8 type; };
 
 // MODE 0: uniform scheme, 1: sparse overrides (per-symbol correction rows), 2: dense table (K x K bytes of M - sim)
 // MAXLEN: longest word the instantiation accepts (32, or 64 for the block-wise wide build)
-template <int MODE, int MAXLEN = NWAP_MAXLEN_FAST>
+// CW: strip width in columns.  NWAP_TAB_CW = NWAP_C / 2 gives the table-driven flavour half-width strips (output stage
+// and sorted-column arrays 48 KB smaller: room for two CTAs per SM next to the row-pair profiles) -- measured: -5.6 %
+// while its 168 registers keep it at one CTA per SM anyway, so the default is the full width.
+#ifndef NWAP_TAB_CW
+#define NWAP_TAB_CW NWAP_C
+#endif
+template <int MODE, int MAXLEN = NWAP_MAXLEN_FAST, int CW = (MODE == 2 ? NWAP_TAB_CW : NWAP_C)>
 struct nwap_tile_smem_t {
-    alignas(16) uint8_t out[NWAP_R * NWAP_PITCH];
+    static constexpr int C = CW;                 // columns per strip
+    static constexpr int PITCH = CW + 16;        // bytes per staged output row (multiple of 16)
+    static_assert(CW % (4 * NWAP_THREADS) == 0 && CW <= NWAP_C && NWAP_C % CW == 0, "strip width");
+    alignas(16) uint8_t out[NWAP_R * PITCH];
     typedef typename nwap_sym_of<MODE>::type sym_t;
     alignas(16) sym_t rowsym[NWAP_R][MAXLEN + 1];                // {a*65537, H'[i+1][0] (, override row)} per matrix row
     // first staged record of row rr.  The 8-byte records of a row END at slot MAXLEN (so that the matrix-row loop of
@@ -180,8 +189,8 @@ struct nwap_tile_smem_t {
     __device__ __forceinline__ sym_t *syms(int rr, int la) { return rowsym[rr] + (END_ALIGNED ? MAXLEN - la : 0); }
     alignas(16) nwap_ov_part ov[MODE == 1 ? NWAP_OV_MAXK : 1];      // per-symbol partner table (sparse-override mode)
     alignas(16) nwap_row_meta meta[NWAP_R + 1];                     // one readable record past the band (row prefetch)
-    uint16_t cols[NWAP_C];        // strip-relative column offsets, sorted by length desc
-    uint8_t clen[NWAP_C];         // their lengths
+    uint16_t cols[CW];            // strip-relative column offsets, sorted by length desc
+    uint8_t clen[CW];             // their lengths
     int bins[NWAP_WARPS][MAXLEN + 2];
     short2 kbounds[256];          // sparse-output mode, normalised filter: per-length score bounds
     unsigned long long unit;
@@ -540,18 +549,39 @@ struct alignas(16) nwap_pair_meta {
     int pad0, pad1;
 };
 #define NWAP_TAB2_PAIRS (NWAP_R / 2)
+// Profile entries are 16 bits, E | E' << 8 (every E fits a byte): with 32-bit entries an alphabet of more than 32
+// symbols puts two symbols on one shared-memory bank, and a warp's 32 column symbols then hit such a pair in nine
+// loads out of ten (ncu at 40 symbols: 1.78 wavefronts per load, the shared-memory pipe 86 % busy -- THE bound of this
+// cell).  Two 16-bit entries share a bank WORD, which is a broadcast, so alphabets of up to 64 symbols are
+// conflict-free; the price is one byte permute per packed cell (E | E' << 8  ->  E | E' << 16).
+#ifndef NWAP_TAB2_16
+#define NWAP_TAB2_16 1
+#endif
+#if NWAP_TAB2_16
+typedef uint16_t nwap_prof_t;
+__device__ __forceinline__ uint32_t nwap_prof_load(const char *p) { return __byte_perm((uint32_t)*reinterpret_cast<const uint16_t *>(p), 0u, 0x4140u); }
+#else
+typedef uint32_t nwap_prof_t;
+__device__ __forceinline__ uint32_t nwap_prof_load(const char *p) { return *reinterpret_cast<const uint32_t *>(p); }
+#endif
+// bytes of the profiles of one band, rounded up so that the pair records behind them stay 16-byte aligned
+__host__ __device__ inline size_t nwap_tab2_prof_bytes(int lmax_rows, int K)
+{
+    return ((size_t)sizeof(nwap_prof_t) * NWAP_TAB2_PAIRS * (size_t)lmax_rows * (size_t)K + 15u) & ~size_t(15);
+}
 
 // Both of the lane's columns are scored in the same loop (two independent chains: the load -> subtract -> max3
 // latency of one hides behind the other; these builds run one CTA per SM, so registers are plentiful).
 template <int LB, int QW, class SM>
 __device__ __forceinline__ void nwap_chunk_rows_tab2(SM &sm, const nwap_scheme_consts &sc, const uint32_t (&w0)[QW],
                                                      const uint32_t (&w1)[QW], const nwap_lane_cols &c, int K,
-                                                     int lmax_rows, const uint32_t *wprof, const nwap_pair_meta *pm,
+                                                     int lmax_rows, const nwap_prof_t *wprof, const nwap_pair_meta *pm,
                                                      nwap_lane_stats &ls)
 {
+    constexpr uint32_t ES = sizeof(nwap_prof_t);
     uint32_t ca[LB], cb[LB];                                     // column symbols as byte offsets in a profile row
 #pragma unroll
-    for (int j = 0; j < LB; ++j) { ca[j] = 4u * nwap_byte_of(w0, j); cb[j] = 4u * nwap_byte_of(w1, j); }
+    for (int j = 0; j < LB; ++j) { ca[j] = ES * nwap_byte_of(w0, j); cb[j] = ES * nwap_byte_of(w1, j); }
     const uint32_t kva = c.l0 == LB ? 0xffffffffu : 0u, k1a = c.l0 == LB - 1 ? 0xffffffffu : 0u;
     const uint32_t kvb = c.l1 == LB ? 0xffffffffu : 0u, k1b = c.l1 == LB - 1 ? 0xffffffffu : 0u;
     const uint32_t kposa = (uint32_t)(sc.beta * c.l0) * 65537u, kposb = (uint32_t)(sc.beta * c.l1) * 65537u;
@@ -565,30 +595,30 @@ __device__ __forceinline__ void nwap_chunk_rows_tab2(SM &sm, const nwap_scheme_c
 #pragma unroll
         for (int j = 0; j <= LB; ++j) { Pa[j] = NWAP_BIAS2; Pb[j] = NWAP_BIAS2; }
         uint32_t b0 = NWAP_BIAS2;                                // H'[i-1][0], the same for both halves and both columns
+                                                                 // (H'[i][0] itself is dominated: nwap_dp_row, DOM)
         uint32_t va0 = 0, va1 = 0, vb0 = 0, vb1 = 0;
         int rows = m.lmin;
 #pragma unroll 1
         for (int ph = 0; ph < 2; ++ph) {
 #pragma unroll 1
             for (; rows > 0; --rows) {
-                const uint32_t left0 = b0 + sc.u2;
-                uint32_t lefta = left0, leftb = left0;
-                uint32_t dwa = b0 - *reinterpret_cast<const uint32_t *>(wr + ca[0]);
-                uint32_t dwb = b0 - *reinterpret_cast<const uint32_t *>(wr + cb[0]);
+                uint32_t lefta = 0, leftb = 0;
+                uint32_t dwa = b0 - nwap_prof_load(wr + ca[0]);
+                uint32_t dwb = b0 - nwap_prof_load(wr + cb[0]);
 #pragma unroll
                 for (int j = 1; j <= LB; ++j) {
                     uint32_t na = 0, nb_ = 0;
                     if (j < LB) {
-                        na = Pa[j] - *reinterpret_cast<const uint32_t *>(wr + ca[j]);
-                        nb_ = Pb[j] - *reinterpret_cast<const uint32_t *>(wr + cb[j]);
+                        na = Pa[j] - nwap_prof_load(wr + ca[j]);
+                        nb_ = Pb[j] - nwap_prof_load(wr + cb[j]);
                     }
-                    const uint32_t cura = nwap_vimax3_s16x2(dwa, Pa[j] + sc.u2, lefta);
-                    const uint32_t curb = nwap_vimax3_s16x2(dwb, Pb[j] + sc.u2, leftb);
+                    const uint32_t cura = j == 1 ? nwap_vmaxs2(dwa, Pa[j] + sc.u2) : nwap_vimax3_s16x2(dwa, Pa[j] + sc.u2, lefta);
+                    const uint32_t curb = j == 1 ? nwap_vmaxs2(dwb, Pb[j] + sc.u2) : nwap_vimax3_s16x2(dwb, Pb[j] + sc.u2, leftb);
                     Pa[j] = cura; lefta = cura; dwa = na;
                     Pb[j] = curb; leftb = curb; dwb = nb_;
                 }
-                b0 = left0;
-                wr += 4 * K;
+                b0 += sc.u2;
+                wr += ES * K;
             }
             const uint32_t ta = (Pa[LB >= 2 ? LB - 1 : LB] & k1a) | (Pa[LB >= 3 ? LB - 2 : LB] & ~k1a);
             const uint32_t tb = (Pb[LB >= 2 ? LB - 1 : LB] & k1b) | (Pb[LB >= 3 ? LB - 2 : LB] & ~k1b);
@@ -613,7 +643,7 @@ __device__ __forceinline__ void nwap_chunk_rows_tab2(SM &sm, const nwap_scheme_c
 template <int QMAX, int QW, class SM>
 __device__ __forceinline__ void nwap_run_chunk_tab2(int LB, SM &sm, const nwap_scheme_consts &sc,
                                                     const uint32_t (&w0)[QW], const uint32_t (&w1)[QW],
-                                                    const nwap_lane_cols &c, int K, int lmax_rows, const uint32_t *wprof,
+                                                    const nwap_lane_cols &c, int K, int lmax_rows, const nwap_prof_t *wprof,
                                                     const nwap_pair_meta *pm, nwap_lane_stats &ls)
 {
 #define NWAP_CASE(n)                                                                                       \
@@ -837,8 +867,8 @@ __device__ __forceinline__ void nwap_sparse_row(SM &sm, const nwap_tile_params &
     if (seg <= 0) return;
     const nwap_sparse_out &so = p.sparse;
     if (so.mode == 1 ? so.threshold > 127 : so.gmin > so.gmax) return;       // nothing can be kept
-    const int skew = nwap_meta_skew(m, rr);
-    const uint8_t *rowbase = sm.out + rr * NWAP_PITCH;           // 16-byte aligned; the segment starts at +skew
+    const int skew = nwap_meta_skew<SM::PITCH>(m, rr);
+    const uint8_t *rowbase = sm.out + rr * SM::PITCH;           // 16-byte aligned; the segment starts at +skew
     const int nvec = (skew + seg + 15) >> 4;
     for (int v0 = 0; v0 < nvec; v0 += 32) {
         const int v = v0 + lane;
@@ -926,8 +956,8 @@ k_score_tiles(const nwap_tile_params p)
         for (int w = tid; w < p.ov_K * p.ov_K; w += NWAP_THREADS) sm.etab[w] = p.etab[w];
     }
     // FLAVOR 3, second shape: row-pair profiles and pair records behind the table (dynamic shared memory, sized by the launch)
-    uint32_t *const tab2_prof = reinterpret_cast<uint32_t *>(sm.etab + (((size_t)p.ov_K * p.ov_K + 15u) & ~size_t(15)));
-    nwap_pair_meta *const tab2_pm = reinterpret_cast<nwap_pair_meta *>(tab2_prof + (size_t)NWAP_TAB2_PAIRS * p.tab2_lmax * p.ov_K);
+    nwap_prof_t *const tab2_prof = reinterpret_cast<nwap_prof_t *>(sm.etab + (((size_t)p.ov_K * p.ov_K + 15u) & ~size_t(15)));
+    nwap_pair_meta *const tab2_pm = reinterpret_cast<nwap_pair_meta *>(reinterpret_cast<char *>(tab2_prof) + nwap_tab2_prof_bytes(p.tab2_lmax, p.ov_K));
     if (CMP && p.sparse.mode == 2)
         for (int b = tid; b < 256; b += NWAP_THREADS) sm.kbounds[b] = p.sparse.bounds[b];
     const nwap_sparse_consts skc = nwap_make_sparse_consts(p.sparse);
@@ -951,8 +981,9 @@ k_score_tiles(const nwap_tile_params p)
 
         int64_t group, strip;
         nwap_unit_decode(p.us, p.unit_begin + t, &group, &strip);
-        const int64_t strip_lo = strip * NWAP_C;
-        const int64_t strip_hi = min(strip_lo + (int64_t)NWAP_C, p.n);
+        constexpr int CW = smem_t::C;                    // strip width of this build (p.us was laid out for it)
+        const int64_t strip_lo = strip * CW;
+        const int64_t strip_hi = min(strip_lo + (int64_t)CW, p.n);
         const int64_t grow0 = group * (int64_t)p.us.gb * NWAP_R;
         const int64_t rmin = max(grow0, p.r_first);
         const int64_t rmax = min(grow0 + (int64_t)p.us.gb * NWAP_R - 1, p.r_last);
@@ -963,11 +994,15 @@ k_score_tiles(const nwap_tile_params p)
         // ---- counting sort of the unit's columns by word length, longest first ----
         for (int b = tid; b < NWAP_WARPS * (SYMLEN + 2); b += NWAP_THREADS) (&sm.bins[0][0])[b] = 0;
         __syncthreads();
-        constexpr int PER = NWAP_C / NWAP_THREADS;     // 16 columns per thread
+        constexpr int PER = CW / NWAP_THREADS;         // 16 columns per thread (8 with half-width strips)
+        static_assert(PER == 16 || PER == 8, "one aligned uint4 / uint2 of lengths per thread");
         uint32_t lw[PER / 4];
-        {
+        if constexpr (PER == 16) {
             const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p.lens + strip_lo) + tid);
             lw[0] = v.x; lw[1] = v.y; lw[2] = v.z; lw[3] = v.w;
+        } else {
+            const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p.lens + strip_lo) + tid);
+            lw[0] = v.x; lw[1] = v.y;
         }
         const int kbase = tid * PER;
         const int win_lo = (int)(cwin_lo - strip_lo), win_hi = (int)(strip_hi - strip_lo);
@@ -975,7 +1010,7 @@ k_score_tiles(const nwap_tile_params p)
         // valid for some of its rows only.  They are sorted BEHIND all the others (bin 0), so that every chunk of the
         // clean part [0, nclean) is valid for every row of every band of the unit and takes the fast path; the few
         // chunks behind it (at most gb * 16 columns) take the path with per-lane range checks.
-        const int dirty_hi = (int)max((int64_t)0, min((int64_t)NWAP_C, grow0 + (int64_t)p.us.gb * NWAP_R - strip_lo));
+        const int dirty_hi = (int)max((int64_t)0, min((int64_t)CW, grow0 + (int64_t)p.us.gb * NWAP_R - strip_lo));
         // zero the lengths of columns outside the window (and clamp, defensively)
 #pragma unroll
         for (int e = 0; e < PER; ++e) {
@@ -1031,7 +1066,7 @@ k_score_tiles(const nwap_tile_params p)
                         m.seglen = (int)(chi - clo);
                         m.g0 = nwap_before_row(r, p.n) + (clo - r - 1) - p.start;
                         const int skew = (int)((reinterpret_cast<uintptr_t>(p.out) + (uintptr_t)m.g0) & 15u);
-                        m.rowadj = tid * NWAP_PITCH + skew - m.clo_off;
+                        m.rowadj = tid * smem_t::PITCH + skew - m.clo_off;
                         m.symend = (uint32_t)(-8 * m.la);
                         m.ala2 = (uint32_t)(sc.alpha * m.la * 65537);
                         if (OV) {
@@ -1077,8 +1112,8 @@ k_score_tiles(const nwap_tile_params p)
                     const uint32_t a0 = i < la0 ? (uint32_t)p.ids[r0 * p.qpad + i] : 0u;
                     const uint32_t a1 = i < la1 ? (uint32_t)p.ids[r1 * p.qpad + i] : 0u;
                     const uint8_t *e0 = sm.etab + a0 * K, *e1 = sm.etab + a1 * K;
-                    uint32_t *w = tab2_prof + (size_t)item * K;
-                    for (int b = 0; b < K; ++b) w[b] = (uint32_t)e0[b] | ((uint32_t)e1[b] << 16);
+                    nwap_prof_t *w = tab2_prof + (size_t)item * K;
+                    for (int b = 0; b < K; ++b) w[b] = (nwap_prof_t)((uint32_t)e0[b] | ((uint32_t)e1[b] << (4 * sizeof(nwap_prof_t))));
                 }
             }
             if (tid == 0) sm.next_chunk = 0;
@@ -1170,8 +1205,8 @@ k_score_tiles(const nwap_tile_params p)
             for (int rr = warp; rr < NWAP_R; rr += NWAP_WARPS) {
                 const int seg = sm.meta[rr].seglen;
                 if (seg <= 0) continue;
-                const int skew = nwap_meta_skew(sm.meta[rr], rr);
-                const uint8_t *src = sm.out + rr * NWAP_PITCH + skew;
+                const int skew = nwap_meta_skew<smem_t::PITCH>(sm.meta[rr], rr);
+                const uint8_t *src = sm.out + rr * smem_t::PITCH + skew;
                 int8_t *dst = p.out + sm.meta[rr].g0;
                 int head = (16 - skew) & 15;
                 if (head > seg) head = seg;
