@@ -200,6 +200,7 @@ struct nwap_tile_smem_t {
     int ncols;                    // sorted columns of the unit: [0, nclean) by length, longest first; [nclean, ncols) unsorted
     int nclean;
     int next_chunk;
+    uint8_t t2order[NWAP_R];      // FLAVOR 3, second shape: the band's rows in order of length (rows are paired by length)
     // dense-table mode: K x K bytes of M - sim.  LAST member: the launch sizes the dynamic shared memory to the
     // alphabet actually used (nwap_tile_smem_bytes), so that tables of up to ~100 symbols leave room for two CTAs per SM
     alignas(16) uint8_t etab[MODE == 2 ? NWAP_TAB_MAXK * NWAP_TAB_MAXK : 16];
@@ -528,6 +529,40 @@ __device__ __forceinline__ void nwap_run_chunk_h(int LB, SM &sm, const nwap_sche
 }
 
 
+// shared-window loads by 32-bit address: one induction variable serves both the load and the loop test (with
+// generic pointers ptxas keeps two copies of it, one per use)
+__device__ __forceinline__ uint2 nwap_lds64(uint32_t addr)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t nwap_lds32(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint4 nwap_lds128(uint32_t addr)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+// cnt += STEP; returns the carry-out (ptxas: one IADD3 with a predicate destination that the loop branch uses)
+template <int STEP>
+__device__ __forceinline__ bool nwap_bump_carry(uint32_t &cnt)
+{
+    uint32_t c;
+    asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, 0, 0;" : "+r"(cnt), "=r"(c) : "n"(STEP));
+    return c != 0;
+}
+__device__ __forceinline__ void nwap_sts8(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.shared.u8 [%0], %1;" :: "r"(addr), "r"(v));
+}
+
+
 // ---- table-driven cell, second shape (FLAVOR 3, round 2): ONE shared-memory load per packed cell -----------------
 // nwap_dp_row_tab packs two COLUMN words against one row word, so a packed cell needs two table entries of the same
 // table row, E[a_i][b0_j] and E[a_i][b1_j]: two LDS.U8, and the shared-memory pipe is the bound (9.3 TCUPS).  Here the
@@ -676,39 +711,6 @@ __device__ __forceinline__ void nwap_run_chunk_tab2(int LB, SM &sm, const nwap_s
 #ifndef NWAP_F2_DUFF_MAXLB
 #define NWAP_F2_DUFF_MAXLB 8
 #endif
-// shared-window loads by 32-bit address: one induction variable serves both the load and the loop test (with
-// generic pointers ptxas keeps two copies of it, one per use)
-__device__ __forceinline__ uint2 nwap_lds64(uint32_t addr)
-{
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ uint32_t nwap_lds32(uint32_t addr)
-{
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ uint4 nwap_lds128(uint32_t addr)
-{
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
-}
-// cnt += STEP; returns the carry-out (ptxas: one IADD3 with a predicate destination that the loop branch uses)
-template <int STEP>
-__device__ __forceinline__ bool nwap_bump_carry(uint32_t &cnt)
-{
-    uint32_t c;
-    asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, 0, 0;" : "+r"(cnt), "=r"(c) : "n"(STEP));
-    return c != 0;
-}
-__device__ __forceinline__ void nwap_sts8(uint32_t addr, uint32_t v)
-{
-    asm volatile("st.shared.u8 [%0], %1;" :: "r"(addr), "r"(v));
-}
-
 template <int LB, int FLAVOR, int QW, class SM>
 __device__ __forceinline__ void nwap_chunk_rows_fast2(SM &sm, const nwap_scheme_consts &sc, const uint32_t (&w0)[QW],
                                                       const uint32_t (&w1)[QW], const nwap_lane_cols &c,
@@ -1101,12 +1103,30 @@ k_score_tiles(const nwap_tile_params p)
             const bool clip_first = p.r_first >= rb0 && p.r_first < rb0 + NWAP_R && p.c_start > strip_lo;
             const bool clip_last = p.r_last >= rb0 && p.r_last < rb0 + NWAP_R && p.c_end + 1 < strip_hi;
             const bool band_simple = rb0 >= rmin && rb0 + NWAP_R - 1 <= rmax && !clip_first && !clip_last;
-            if (FLAVOR == 3 && p.tab2_lmax > 0 && band_simple) {
+            // FLAVOR 3, second shape: the band's rows are PAIRED BY LENGTH (a pair runs max(la, la') matrix rows for both
+            // of its words: neighbours in the vocabulary waste 19 % of them at the French length distribution, neighbours
+            // in length order 3 %).  Every warp ranks the 16 lengths for itself (lanes 0..15, shuffles only): t2row =
+            // the band row whose length has rank `lane`, longest first, ties by row.
+            const bool tab2_band = FLAVOR == 3 && p.tab2_lmax > 0 && band_simple;
+            if (tab2_band) {
+                // sm.t2order[k] = the band row whose length has rank k (longest first, ties by row)
+                if (tid < NWAP_R) {
+                    const uint8_t *bl = p.lens + rb0;
+                    const int mylen = (int)bl[tid];
+                    int rank = 0;
+#pragma unroll
+                    for (int j = 0; j < NWAP_R; ++j) {
+                        const int lj = (int)bl[j];
+                        rank += (lj > mylen || (lj == mylen && j < tid)) ? 1 : 0;
+                    }
+                    sm.t2order[rank] = (uint8_t)tid;
+                }
+                __syncthreads();
                 // row-pair profiles of the band (nwap_chunk_rows_tab2): one (pair, matrix row) per thread
                 const int lmx = p.tab2_lmax, K = p.ov_K;
                 for (int item = tid; item < NWAP_TAB2_PAIRS * lmx; item += NWAP_THREADS) {
                     const int pr = item / lmx, i = item - pr * lmx;
-                    const int64_t r0 = rb0 + 2 * pr, r1 = r0 + 1;
+                    const int64_t r0 = rb0 + sm.t2order[2 * pr], r1 = rb0 + sm.t2order[2 * pr + 1];
                     const int la0 = (int)p.lens[r0], la1 = (int)p.lens[r1];
                     if (i >= max(la0, la1)) continue;
                     const uint32_t a0 = i < la0 ? (uint32_t)p.ids[r0 * p.qpad + i] : 0u;
@@ -1118,9 +1138,9 @@ k_score_tiles(const nwap_tile_params p)
             }
             if (tid == 0) sm.next_chunk = 0;
             __syncthreads();
-            if (FLAVOR == 3 && p.tab2_lmax > 0 && band_simple) {
+            if (tab2_band) {
                 if (tid < NWAP_TAB2_PAIRS) {
-                    const nwap_row_meta &m0 = sm.meta[2 * tid], &m1 = sm.meta[2 * tid + 1];
+                    const nwap_row_meta &m0 = sm.meta[sm.t2order[2 * tid]], &m1 = sm.meta[sm.t2order[2 * tid + 1]];
                     nwap_pair_meta pm;
                     pm.lmin = min(m0.la, m1.la); pm.lmax = max(m0.la, m1.la);
                     pm.sel = m0.la <= m1.la ? 0x0000ffffu : 0xffff0000u;
