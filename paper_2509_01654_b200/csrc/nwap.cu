@@ -67,7 +67,8 @@ struct device_guard {
 #define ON_DEVICE(dev) device_guard guard_(dev); CK(guard_.err)
 
 static_assert(sizeof(nwap_dev_stats) == sizeof(nwap_stats), "stats layouts must agree");
-static_assert(sizeof(nwap_tile_smem_t<1>) <= 227 * 1024 && sizeof(nwap_tile_smem_t<2>) <= 227 * 1024, "tile shared memory too large");
+static_assert(sizeof(nwap_tile_smem_t<1>) <= 227 * 1024 && sizeof(nwap_tile_smem_t<2>) <= 227 * 1024 &&
+              sizeof(nwap_tile_smem_t<2, NWAP_MAXLEN_WIDE>) <= 227 * 1024, "tile shared memory too large");
 static_assert(2 * sizeof(nwap_tile_smem_t<0, NWAP_MAXLEN_WIDE>) <= 226 * 1024, "the wide build must keep two CTAs per SM");
 
 }  // namespace
@@ -81,18 +82,25 @@ nwap_tile_kernel_t nwap_tile_kernel(int family, int qclass)
     case 5: return nwap_tiles_wide(false);
     case 6: return nwap_tiles_cmp(qclass);
     case 7: return nwap_tiles_wide(true);
+    case 8: return nwap_tiles_tabcmp(qclass);
+    case 9: return nwap_tiles_tabwide(false);
+    case 10: return nwap_tiles_tabwide(true);
     default: return nwap_tiles_f1(qclass);
     }
 }
+
+typedef nwap_tile_smem_t<2, NWAP_MAXLEN_WIDE> nwap_tile_smem_wide_tab;
+static bool nwap_family_is_tab(int family) { return family == 4 || family >= 8; }
 
 size_t nwap_tile_smem_bytes(int family, int K)
 {
     switch (family) {
     case 3: return sizeof(nwap_tile_smem_t<1>);
-    case 4: {
+    case 4: case 8: case 9: case 10: {
         // the K x K table is the struct's last member: K = 0 asks for the largest alphabet
         const size_t tab = K > 0 ? (((size_t)K * (size_t)K + 15u) & ~size_t(15)) : (size_t)NWAP_TAB_MAXK * NWAP_TAB_MAXK;
-        return offsetof(nwap_tile_smem_t<2>, etab) + std::max<size_t>(16, tab);
+        const size_t base = family >= 9 ? offsetof(nwap_tile_smem_wide_tab, etab) : offsetof(nwap_tile_smem_t<2>, etab);
+        return base + std::max<size_t>(16, tab);
     }
     case 5: case 7: return sizeof(nwap_tile_smem_t<0, NWAP_MAXLEN_WIDE>);
     default: return sizeof(nwap_tile_smem_t<0>);
@@ -195,7 +203,7 @@ int ensure_device_cache(int device, device_cache **out)
                 nwap_tile_kernel_t k = nwap_tile_kernel(f, w);
                 const size_t smem = nwap_tile_smem_bytes(f);
                 // the table flavour's launch adds its row-pair profiles (enqueue_score): allow it the whole SM
-                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, f == 4 ? 226 * 1024 : (int)smem));
+                CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, nwap_family_is_tab(f) ? 226 * 1024 : (int)smem));
                 int occ = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NWAP_THREADS, smem));
                 dc.occ_tiles[f * 3 + w] = occ;
@@ -282,7 +290,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     const bool uniform_ok = !c->general || c->sparse_ov;
     const bool fast_ok = uniform_ok && c->qmax <= NWAP_MAXLEN_FAST;
     const bool wide_ok = !c->general && c->qmax <= NWAP_MAXLEN_WIDE;          // block-wise path: uniform schemes only
-    const bool tab_ok = c->general && c->tab_ok && c->qmax <= NWAP_MAXLEN_FAST;
+    const bool tab_ok = c->general && c->tab_ok && c->qmax <= NWAP_MAXLEN_WIDE;   // words over 32 symbols: the wide build of the table cell
     const bool sym_ok = fast_ok && !c->general && nwap_flavor2_ok(c->match, c->mismatch);
     // PACKED3 (2 DPX + IMAD + IADD) is ~8 % faster than PACKED (2 DPX + 2 IMAD) and ~14 % faster than PACKED_SYM
     // (2 DPX + IADD3: one issue fewer, but IADD3 shares the DPX pipe): profiles/r01f_ab_packed_sym.txt
@@ -293,7 +301,7 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     if (variant == NWAP_VARIANT_AUTO)
         variant = tab_ok ? NWAP_VARIANT_PACKED_TAB : (fast_ok || wide_ok) ? NWAP_VARIANT_PACKED3 : NWAP_VARIANT_SIMPLE;
     if (variant == NWAP_VARIANT_PACKED_TAB && !tab_ok)
-        return fail(NWAP_EINVAL, "packed_tab kernel needs a similarity table (overrides) with K <= %d and max word length <= %d", NWAP_TAB_MAXK, NWAP_MAXLEN_FAST);
+        return fail(NWAP_EINVAL, "packed_tab kernel needs a similarity table (overrides) with K <= %d and max word length <= %d", NWAP_TAB_MAXK, NWAP_MAXLEN_WIDE);
     if (variant == NWAP_VARIANT_PACKED_SYM && !sym_ok)
         return fail(NWAP_EINVAL, "packed_sym kernel needs a uniform scheme with match >= mismatch and max word length <= %d (have %d%s)",
                     NWAP_MAXLEN_FAST, c->qmax, c->general ? ", similarity overrides" : "");
@@ -303,8 +311,8 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     if (variant == NWAP_VARIANT_PACKED3 && !fast_ok && !wide_ok)
         return fail(NWAP_EINVAL, "packed kernel needs a uniform scheme and max word length <= %d, or at most %d overrides per symbol and max word length <= %d (have %d%s)",
                     NWAP_MAXLEN_WIDE, NWAP_MAX_OV, NWAP_MAXLEN_FAST, c->qmax, c->general ? ", similarity table" : "");
-    if (sparse && (variant != NWAP_VARIANT_PACKED3 || c->general))
-        return fail(NWAP_EINVAL, "sparse output is built for the default packed kernel and uniform schemes");
+    if (sparse && !((variant == NWAP_VARIANT_PACKED3 && !c->general) || variant == NWAP_VARIANT_PACKED_TAB))
+        return fail(NWAP_EINVAL, "sparse output is built for the default packed kernel (uniform schemes) and the table-driven kernel (override schemes)");
 
     if (variant == NWAP_VARIANT_SIMPLE) {
         nwap_simple_params p;
@@ -325,9 +333,10 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     const bool tab = variant == NWAP_VARIANT_PACKED_TAB;
     const bool ov = c->general && !tab;               // here: general and not tab implies sparse_ov
     const int flavor = tab ? 3 : variant == NWAP_VARIANT_PACKED_SYM ? 2 : (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
-    const bool wide = flavor == 1 && !ov && c->qmax > NWAP_WIDE_FROM;
+    const bool wide = (flavor == 1 || flavor == 3) && !ov && c->qmax > NWAP_WIDE_FROM;
     const int qclass = wide ? 1 : c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
-    const int family = wide ? (sparse ? 7 : 5) : sparse ? 6 : ov ? 3 : tab ? 4 : flavor;
+    const int family = tab ? (wide ? (sparse ? 10 : 9) : sparse ? 8 : 4)
+                           : wide ? (sparse ? 7 : 5) : sparse ? 6 : ov ? 3 : flavor;
     nwap_tile_params p;
     p.ids = c->d_ids; p.lens = c->d_lens; p.n = c->n; p.qpad = c->qpad;
     p.start = start; p.end = end;

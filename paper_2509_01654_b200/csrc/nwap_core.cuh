@@ -405,18 +405,18 @@ inline bool nwap_build_ov_table(const int8_t *sim, int K, int match, int mismatc
 //     dw = diag - (E[a_i][b0_j] | E[a_i][b1_j] << 16)
 // (non-negative halves subtracted from biased halves: no borrow crosses).  Two byte loads per packed cell replace
 // the compare + multiply; c0/c1 hold the lane's column symbols as byte offsets.
-template <int LB>
+template <int LB, bool DOM = true>
 NWAP_HD void nwap_dp_row_tab(uint32_t rowoff, const uint32_t *c0, const uint32_t *c1, uint32_t (&P)[LB + 1],
-                             uint32_t d0, const nwap_scheme_consts &sc, const uint8_t *etab)
+                             uint32_t d0, const nwap_scheme_consts &sc, const uint8_t *etab, uint32_t left0 = 0u)
 {
     const uint8_t *row = etab + rowoff;
-    uint32_t left = 0;                                      // column 1: the boundary is dominated (nwap_dp_row, DOM)
+    uint32_t left = left0;                                  // DOM (matrix border): column 1's boundary is dominated (nwap_dp_row)
     uint32_t dw = d0 - ((uint32_t)row[c0[0]] | ((uint32_t)row[c1[0]] << 16));
 #pragma unroll
     for (int j = 1; j <= LB; ++j) {
         uint32_t dw_next = 0;
         if (j < LB) dw_next = P[j] - ((uint32_t)row[c0[j]] | ((uint32_t)row[c1[j]] << 16));
-        const uint32_t cur = j == 1 ? nwap_vmaxs2(dw, P[j] + sc.u2) : nwap_vimax3_s16x2(dw, P[j] + sc.u2, left);
+        const uint32_t cur = (DOM && j == 1) ? nwap_vmaxs2(dw, P[j] + sc.u2) : nwap_vimax3_s16x2(dw, P[j] + sc.u2, left);
         P[j] = cur;
         left = cur;
         dw = dw_next;
@@ -483,6 +483,50 @@ NWAP_HD uint32_t nwap_dp_blocks(const nwap_sym2 *row_sym2, int la, const uint8_t
             nwap_dp_row<NWAP_WB, 1>(x.a2, nb, P, d0, left0, sc);
             d0 = left0;
             save[i] = P[NWAP_WB];                                  // H'[i+1][WB*(blk+1)] for the next block
+        }
+        const int j0 = l0 - NWAP_WB * blk, j1 = l1 - NWAP_WB * blk;
+#pragma unroll
+        for (int j = 1; j <= NWAP_WB; ++j) {
+            if (j == j0) lo = P[j] & 0xffffu;
+            if (j == j1) hi = P[j] & 0xffff0000u;
+        }
+    }
+    return lo | hi;
+}
+
+// The same block-wise scoring with the table-driven cell (FLAVOR 3: row_sym2[i].a2 is the row offset a_i * K in the
+// K x K table of M - sim): override schemes over words of up to 64 symbols stay on the packed kernel.
+NWAP_HD uint32_t nwap_dp_blocks_tab(const nwap_sym2 *row_sym2, int la, const uint8_t *b0, const uint8_t *b1, int nblk,
+                                    int l0, int l1, const nwap_scheme_consts &sc, uint32_t *save, const uint8_t *etab)
+{
+    uint32_t lo = 0, hi = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+        uint32_t c0[NWAP_WB], c1[NWAP_WB];
+#if defined(__CUDA_ARCH__)
+        {
+            const uint4 x = __ldg(reinterpret_cast<const uint4 *>(b0 + NWAP_WB * blk));
+            const uint4 y = __ldg(reinterpret_cast<const uint4 *>(b1 + NWAP_WB * blk));
+            const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, yw[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int j = 0; j < NWAP_WB; ++j) {
+                c0[j] = (xw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+                c1[j] = (yw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+            }
+        }
+#else
+        for (int j = 0; j < NWAP_WB; ++j) { c0[j] = b0[NWAP_WB * blk + j]; c1[j] = b1[NWAP_WB * blk + j]; }
+#endif
+        uint32_t P[NWAP_WB + 1];
+#pragma unroll
+        for (int j = 0; j <= NWAP_WB; ++j) P[j] = NWAP_BIAS2;      // H'[0][j]
+        uint32_t d0 = NWAP_BIAS2;                                  // H'[0][WB*blk]
+#pragma unroll 1
+        for (int i = 0; i < la; ++i) {
+            const nwap_sym2 x = row_sym2[i];
+            const uint32_t left0 = blk == 0 ? x.d0 + sc.u2 : save[i]; // H'[i+1][WB*blk]
+            nwap_dp_row_tab<NWAP_WB, false>(x.a2, c0, c1, P, d0, sc, etab, left0);
+            d0 = left0;
+            save[i] = P[NWAP_WB];
         }
         const int j0 = l0 - NWAP_WB * blk, j1 = l1 - NWAP_WB * blk;
 #pragma unroll

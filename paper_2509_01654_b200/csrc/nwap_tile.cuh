@@ -823,7 +823,7 @@ __device__ __forceinline__ void nwap_stage_sym(nwap_sym8 &, uint32_t, const nwap
 #else
 #define NWAP_WIDE_ATTR __noinline__
 #endif
-template <class SM>
+template <int FLAVOR, class SM>
 __device__ NWAP_WIDE_ATTR void nwap_run_chunk_wide(int LB, SM &sm, const nwap_scheme_consts &sc, const uint8_t *b0,
                                                  const uint8_t *b1, const nwap_lane_cols &c, bool fast, int want_hist,
                                                  nwap_lane_stats &ls)
@@ -836,7 +836,9 @@ __device__ NWAP_WIDE_ATTR void nwap_run_chunk_wide(int LB, SM &sm, const nwap_sc
         const nwap_row_meta &m = sm.meta[rr];
         const int la = m.la;
         if (la == 0) continue;
-        const uint32_t v = nwap_dp_blocks(reinterpret_cast<const nwap_sym2 *>(sm.syms(rr, la)), la, b0, b1, nblk, c.l0, c.l1, sc, save);
+        const nwap_sym2 *rs = reinterpret_cast<const nwap_sym2 *>(sm.syms(rr, la));
+        const uint32_t v = FLAVOR == 3 ? nwap_dp_blocks_tab(rs, la, b0, b1, nblk, c.l0, c.l1, sc, save, sm.etab)
+                                       : nwap_dp_blocks(rs, la, b0, b1, nblk, c.l0, c.l1, sc, save);
         nwap_emit(sm, m, m.ala2, m.rowadj, v, c, fast, want_hist, ls, ca);
     }
     nwap_close_chunk(ls, ca);
@@ -948,7 +950,7 @@ k_score_tiles(const nwap_tile_params p)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const nwap_scheme_consts sc = p.sc;
     constexpr int QW = QMAX <= 16 ? 4 : 8;
-    static_assert(!WIDE || (FLAVOR == 1 && !OV && QMAX == 24), "the wide build exists for the default uniform-scheme cell only");
+    static_assert(!WIDE || ((FLAVOR == 1 || FLAVOR == 3) && !OV && QMAX == 24), "the wide build exists for the default uniform-scheme cell and the table-driven cell");
 
     if (tid == 0) { sm.sum = 0; sm.count = 0; sm.mn = 127; sm.mx = -128; }
     // the 256-bin histogram is not accumulated here: a request for it is served by k_payload_stats over the
@@ -1187,7 +1189,7 @@ k_score_tiles(const nwap_tile_params p)
                 const int mixmode = min(LB - lmin, 3);      // 0: uniform, 1/2: last two/three columns, 3: deep
                 const bool fast = band_simple && clean;
                 if (WIDE && LB > QMAX) {
-                    nwap_run_chunk_wide(LB, sm, sc, p.ids + ca * p.qpad, p.ids + cb * p.qpad, cA, fast, kNoHist, ls);
+                    nwap_run_chunk_wide<FLAVOR>(LB, sm, sc, p.ids + ca * p.qpad, p.ids + cb * p.qpad, cA, fast, kNoHist, ls);
                     continue;
                 }
                 if (FLAVOR == 3) {
@@ -1274,9 +1276,10 @@ k_score_tiles(const nwap_tile_params p)
 // Tile-kernel instantiations live in their own translation units (tiles_*.cu, compiled in parallel); the ABI
 // unit fetches them through this getter.  family: 0 = FLAVOR 0, 1 = FLAVOR 1 (default), 2 = FLAVOR 2,
 // 3 = sparse overrides, 4 = dense table, 5 = wide (words up to 64 symbols), 6 = sparse output, 7 = wide + sparse
-// output.  qclass: 0/1/2 = register row width 16/24/32 (ignored by the wide families).
+// output, 8 = dense table + sparse output, 9 = dense table, wide, 10 = dense table, wide + sparse output.
+// qclass: 0/1/2 = register row width 16/24/32 (ignored by the wide families).
 typedef void (*nwap_tile_kernel_t)(const nwap_tile_params);
-#define NWAP_TILE_FAMILIES 8
+#define NWAP_TILE_FAMILIES 11
 nwap_tile_kernel_t nwap_tile_kernel(int family, int qclass);
 size_t nwap_tile_smem_bytes(int family, int K = 0);
 nwap_tile_kernel_t nwap_tiles_f0f2(int family, int qclass);
@@ -1284,4 +1287,6 @@ nwap_tile_kernel_t nwap_tiles_f1(int qclass);
 nwap_tile_kernel_t nwap_tiles_ov(int qclass);
 nwap_tile_kernel_t nwap_tiles_tab(int qclass);
 nwap_tile_kernel_t nwap_tiles_wide(bool cmp);
+nwap_tile_kernel_t nwap_tiles_tabcmp(int qclass);
+nwap_tile_kernel_t nwap_tiles_tabwide(bool cmp);
 nwap_tile_kernel_t nwap_tiles_cmp(int qclass);

@@ -503,7 +503,7 @@ def test_dense_similarity_tables_on_the_packed_kernel():
                 got, st = _score(ctx, 0, nw.num_edges(n), v)
                 assert np.array_equal(got, ref), (K, v)
                 assert st[:4] == (rsum, rmin, rmax, nw.num_edges(n))
-    # words over 32 symbols with an override scheme: the generic kernel
+    # words over 32 symbols with an override scheme: the wide build of the table-driven cell (was: the generic kernel)
     K, n, q = 12, 300, 40
     ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
     lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
@@ -511,10 +511,11 @@ def test_dense_similarity_tables_on_the_packed_kernel():
     scheme = nw.ScoringScheme(1, -1, -1, overrides={(0, 1): 0, (2, 3): 1})
     ref, *_ = _oracle(ids, lens, scheme, 0, nw.num_edges(n))
     with NwapContext(ids, lens, scheme) as ctx:
-        got, _ = _score(ctx, 0, nw.num_edges(n), "auto")
-        assert np.array_equal(got, ref)
-        with pytest.raises(ValueError, match="packed_tab"):
-            ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed_tab")
+        for v in ("auto", "packed_tab", "simple"):
+            got, _ = _score(ctx, 0, nw.num_edges(n), v)
+            assert np.array_equal(got, ref), v
+        with pytest.raises(ValueError, match="packed kernel"):      # the compare-based override cell stays at 32 symbols
+            ctx.score_range(0, 10, torch.empty(10, dtype=torch.int8, device="cuda"), variant="packed3")
 
 
 # ---- BASELINE.json configs -------------------------------------------------------------------

@@ -210,3 +210,92 @@ def test_all_words_at_the_64_symbol_limit():
         st = ctx.score_range(0, P, out)
         assert np.array_equal(out.cpu().numpy(), ref)
         assert st[:4] == (rsum, rmin, rmax, P)
+
+
+# ------------------------------------------------------------- override schemes: long words, sparse output
+
+def _override_scheme(rng, K, q, gap, dense):
+    """A random override scheme the int8 preflight admits for words of up to q symbols (engine.py:72-96)."""
+    lim = 127 // q
+    if dense:
+        lo_s, hi_s = -min(2, 128 // q), min(2, lim)
+        ov = {(a, b): int(rng.integers(lo_s, hi_s + 1)) for a in range(K) for b in range(a, K)}
+        return nw.ScoringScheme(ov[(0, 0)], ov[(0, 1)], gap, overrides=ov)
+    m, x = min(1, lim), -1
+    ov = {}
+    for _ in range(6):
+        a_, b_ = int(rng.integers(0, K)), int(rng.integers(0, K))
+        ov[(min(a_, b_), max(a_, b_))] = int(rng.integers(-min(2, 128 // q), min(2, lim) + 1))
+    return nw.ScoringScheme(m, x, gap, overrides=ov)
+
+
+@pytest.mark.parametrize("qmax,K,dense", [(33, 12, False), (48, 40, True), (64, 40, False), (64, 7, True)])
+def test_override_scheme_with_long_words_stays_on_the_packed_kernel(qmax, K, dense):
+    """Override schemes over vocabularies with words of 33..64 symbols ran the generic one-thread-per-pair kernel
+    (0.56 TCUPS); now `auto` takes the wide build of the table-driven cell (block-wise path for the long chunks).
+    All bytes + statistics vs the oracle and vs the generic kernel, misaligned sub-ranges, sparse output."""
+    rng = np.random.default_rng(7000 + qmax + K)
+    n = 5000
+    lens = np.clip(np.rint(rng.normal(8.5, 2.8, size=n)), 1, 24).astype(np.uint8)
+    long_ix = rng.choice(n, size=n // 25, replace=False)
+    lens[long_ix] = rng.integers(25, qmax + 1, size=long_ix.size)
+    lens[rng.integers(0, n)] = qmax
+    ids = rng.integers(0, K, size=(n, qmax)).astype(np.uint8)
+    scheme = _override_scheme(rng, K, qmax, -1, dense)
+    P = nw.num_edges(n)
+    ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P)
+    with NwapContext(ids, lens, scheme) as ctx:
+        out = torch.empty(P, dtype=torch.int8, device="cuda")
+        for variant in ("auto", "packed_tab"):
+            out.fill_(0x55)
+            st = ctx.score_range(0, P, out, variant=variant)
+            got = out.cpu().numpy()
+            bad = np.flatnonzero(got != ref)
+            assert bad.size == 0, (variant, bad[:5], got[bad[:5]], ref[bad[:5]])
+            assert st[:4] == (rsum, rmin, rmax, P)
+        s, e = P // 3 + 7, P // 3 + 7 + 300_001
+        ctx.score_range(s, e, out[5:], variant="simple")
+        assert np.array_equal(out[5: 5 + e - s].cpu().numpy(), ref[s:e])
+        for s, e, off in [(5, 77, 3), (P // 2 + 1, P // 2 + 100_001, 9), (P - 40_000, P, 15)]:
+            buf = torch.full((e - s + 48,), 0x55, dtype=torch.int8, device="cuda")
+            ctx.score_range(s, e, buf[off:])
+            host = buf.cpu().numpy()
+            assert np.array_equal(host[off: off + e - s], ref[s:e])
+            assert (host[:off] == 0x55).all() and (host[off + e - s:] == 0x55).all()
+        thr = int(np.percentile(ref, 99.9))
+        ridx, rsc, rdeg = orc.np_compact(ref, 0, n, thr)
+        degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+        idx, sc, st2 = ctx.score_range_compact(0, P, threshold=thr, capacity=len(ridx), degree=degree)
+        assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
+        assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
+        assert st2 == (rsum, rmin, rmax, P)
+
+
+@pytest.mark.parametrize("K,q,dense", [(40, 24, False), (40, 16, True), (128, 12, True), (9, 32, False)])
+def test_sparse_output_of_an_override_scheme(K, q, dense):
+    """The sparse-output mode of the edge writer on the table-driven kernel: kept list, degree and statistics equal
+    the threshold compaction of the dense payload (numpy model over the oracle's bytes), with and without the dense
+    payload written alongside."""
+    rng = np.random.default_rng(9000 + K + q)
+    n = 4000
+    lens = rng.integers(1, q + 1, size=n).astype(np.uint8)
+    lens[0] = q
+    ids = rng.integers(0, K, size=(n, q)).astype(np.uint8)
+    scheme = _override_scheme(rng, K, q, -2 if q <= 24 else -1, dense)
+    P = nw.num_edges(n)
+    ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P)
+    with NwapContext(ids, lens, scheme) as ctx:
+        for thr in (int(np.percentile(ref, 99.5)), int(ref.max())):
+            ridx, rsc, rdeg = orc.np_compact(ref, 0, n, thr)
+            degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+            idx, sc, st = ctx.score_range_compact(0, P, threshold=thr, capacity=len(ridx) + 5, degree=degree)
+            assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
+            assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
+            assert st == (rsum, rmin, rmax, P)
+        s, e = P // 5 + 3, P // 5 + 3 + 1_000_001
+        thr = int(np.percentile(ref[s:e], 99.0))
+        ridx, rsc, _ = orc.np_compact(ref[s:e], s, n, thr)
+        dense_out = torch.full((e - s,), 0x55, dtype=torch.int8, device="cuda")
+        idx, sc, _ = ctx.score_range_compact(s, e, threshold=thr, capacity=len(ridx), out=dense_out)
+        assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
+        assert np.array_equal(dense_out.cpu().numpy(), ref[s:e])
