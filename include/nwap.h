@@ -40,14 +40,17 @@ extern "C" {
 #define NWAP_ECAPACITY  -5   /* compaction output buffer too small */
 
 /* kernel variants selectable per call (nwap_score_range `variant`) */
-#define NWAP_VARIANT_AUTO    0  /* packed DPX tile kernel when the scheme/store allow it, else simple; a uniform scheme
-                                 * always allows it: words of 33..64 symbols (gap -1, engine.py:83-90) run the wide build */
-#define NWAP_VARIANT_SIMPLE  1  /* one thread per pair, int32 cells, K x K table: any scheme, any q <= 255 */
+#define NWAP_VARIANT_AUTO    0  /* the packed DPX tile kernel: PACKED3 for a uniform scheme, PACKED_TAB for an override
+                                 * scheme; words of 33..64 symbols (gap -1, engine.py:83-90) run the wide build of either.
+                                 * Every scheme and store the uint8 word store and the preflight admit is served there. */
+#define NWAP_VARIANT_SIMPLE  1  /* one thread per pair, int32 cells, K x K table: any scheme, any q <= 255; the independent
+                                 * second implementation the packed kernel is cross-checked against */
 #define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 DPX + 2 IMAD per packed cell */
 #define NWAP_VARIANT_PACKED3 3  /* s16x2 DPX tile kernel, 2 DPX + 1 IMAD + 1 IADD per packed cell; word length <= 64
                                  * (chunks longer than 24 symbols are scored block-wise, 16 columns at a time) */
 #define NWAP_VARIANT_PACKED_TAB 5 /* s16x2 DPX tile kernel with a K x K similarity table in shared memory (K <= 256):
-                                   * any override table; 2 byte loads per packed cell instead of compare + multiply */
+                                   * any override table, word length <= 64; one 16-bit load from a row-pair profile (or
+                                   * two byte loads from the table) per packed cell instead of compare + multiply */
 #define NWAP_VARIANT_PACKED_SYM 4 /* s16x2 DPX tile kernel, symmetric gap potential: 2 DPX + 1 IADD3 per packed cell
                                    * (needs match >= mismatch and no overrides) */
 
@@ -90,10 +93,9 @@ int nwap_create(nwap_ctx **ctx_out, int device,
 /* ScoringScheme.overrides (aligner.py:51-65, engine.py:113-116): install a
  * dense symmetric K x K similarity table (host int8, row-major).  Symbols >= K
  * are rejected.  The packed tile kernel runs the table through its table-driven flavour
- * (NWAP_VARIANT_PACKED_TAB, what NWAP_VARIANT_AUTO picks; K <= 256, words of up to 32 symbols); a table
- * that is the uniform scheme plus at most 2 overrides per symbol (K <= 128) can also run as corrections
- * of the compare-based cell (NWAP_VARIANT_PACKED3); an override scheme with longer words goes to the
- * generic one-thread-per-pair kernel. */
+ * (NWAP_VARIANT_PACKED_TAB, what NWAP_VARIANT_AUTO picks; K <= 256, words of up to 64 symbols); a table
+ * that is the uniform scheme plus at most 2 overrides per symbol (K <= 128, words of up to 32 symbols) can
+ * also run as corrections of the compare-based cell (NWAP_VARIANT_PACKED3). */
 int nwap_set_similarity(nwap_ctx *ctx, const int8_t *sim, int K);
 
 void nwap_destroy(nwap_ctx *ctx);
@@ -162,8 +164,8 @@ int nwap_compact_range(nwap_ctx *ctx, const int8_t *payload_dev, int64_t start, 
  * restores index order, so the result is identical to nwap_compact_range over the dense payload.
  * degree_dev as for nwap_compact_range (not zeroed here); stats_host (may be NULL) receives the range's
  * sum/min/max/count.  More than `cap` (< 2^31) kept edges: NWAP_ECAPACITY, *count_host is the true count and
- * the output arrays are unspecified.  idx_out_dev doubles as sort scratch.  variant: AUTO or PACKED3, uniform
- * schemes only.  Synchronises `stream`. */
+ * the output arrays are unspecified.  idx_out_dev doubles as sort scratch.  variant: AUTO, PACKED3 (uniform
+ * schemes) or PACKED_TAB (override schemes).  Synchronises `stream`. */
 int nwap_score_range_compact(nwap_ctx *ctx, int64_t start, int64_t end, int8_t *out_dev, int threshold,
                              int64_t *idx_out_dev, int8_t *score_out_dev, int64_t cap, int64_t *count_host,
                              int32_t *degree_dev, nwap_stats *stats_host, int variant, void *stream);

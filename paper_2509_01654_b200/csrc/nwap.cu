@@ -333,7 +333,10 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     const bool tab = variant == NWAP_VARIANT_PACKED_TAB;
     const bool ov = c->general && !tab;               // here: general and not tab implies sparse_ov
     const int flavor = tab ? 3 : variant == NWAP_VARIANT_PACKED_SYM ? 2 : (ov || variant == NWAP_VARIANT_PACKED3) ? 1 : 0;
-    const bool wide = (flavor == 1 || flavor == 3) && !ov && c->qmax > NWAP_WIDE_FROM;
+    // Uniform schemes take the wide build from 25 symbols on: its 24-wide bodies keep the fast2 family and the few
+    // longer chunks go block-wise, which beats the 32-wide instantiation (no fast2, spills) by 29 % on a natural
+    // vocabulary with a 25..32-symbol tail (tools/q32_bench.py).  The table-driven cell keeps its 32-wide build (+5 %).
+    const bool wide = !ov && ((flavor == 1 && c->qmax > NWAP_WIDE_FROM) || (flavor == 3 && c->qmax > NWAP_MAXLEN_FAST));
     const int qclass = wide ? 1 : c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
     const int family = tab ? (wide ? (sparse ? 10 : 9) : sparse ? 8 : 4)
                            : wide ? (sparse ? 7 : 5) : sparse ? 6 : ov ? 3 : flavor;

@@ -36,7 +36,7 @@
 #define NWAP_WARPS (NWAP_THREADS / 32)
 #define NWAP_MAXLEN_FAST 32              // register-resident row limit
 #ifndef NWAP_WIDE_FROM
-#define NWAP_WIDE_FROM 32                // vocabularies whose longest word exceeds this run the wide build
+#define NWAP_WIDE_FROM 24                // uniform schemes: vocabularies whose longest word exceeds this run the wide build
 #endif
 
 struct nwap_dev_stats {                   // same layout as nwap_stats

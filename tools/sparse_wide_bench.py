@@ -92,5 +92,32 @@ for frac in (0.0, 0.001, 0.01):
         out[f"long_tail_{frac}"] = {"ms": t, "gcups": cells / t / 1e6, "pairs_per_s": P / t * 1e3, "qmax": int(lens2.max())}
         print(json.dumps({f"long_tail_{frac}": out[f"long_tail_{frac}"]}), flush=True)
         del buf
+# (4) the same with an OVERRIDE scheme (table-driven cell): long-word tail on its wide build, and its sparse output
+ov = {(0, 1): 0, (2, 5): 1, (3, 4): 0, (7, 9): -1, (10, 11): 0, (0, 6): 1}
+scheme_ov = nw.ScoringScheme(1, -1, -1, overrides=ov)
+for frac in (0.0, 0.001, 0.01):
+    rng = np.random.default_rng(7)
+    lens2 = base_lens.copy()
+    q = 48 if frac else int(base_lens.max())
+    ids2 = np.zeros((len(lens2), q), dtype=np.uint8)
+    ids2[:, : base_ids.shape[1]] = base_ids
+    if frac:
+        pick = rng.choice(len(lens2), size=int(frac * len(lens2)), replace=False)
+        lens2[pick] = rng.integers(33, 49, size=pick.size)
+        ids2[pick] = rng.integers(0, 40, size=(pick.size, q))
+    cells = synth.total_cells(lens2)
+    with NwapContext(ids2, lens2, scheme_ov) as ctx:
+        P = ctx.num_edges
+        buf = torch.empty(P, dtype=torch.int8, device="cuda")
+        t, _ = timed(lambda: ctx.score_range(0, P, buf, sync=False))
+        rec = {"ms": t, "gcups": cells / t / 1e6, "qmax": int(lens2.max())}
+        if not frac:
+            thr = 2
+            kept = int((buf >= thr).sum().item())
+            ts, _ = timed(lambda: ctx.score_range_compact(0, P, threshold=thr, capacity=kept))
+            rec.update({"sparse_thr": thr, "sparse_kept": kept, "sparse_only_ms": ts, "sparse_over_dense": ts / t})
+        out[f"override_long_tail_{frac}"] = rec
+        print(json.dumps({f"override_long_tail_{frac}": rec}), flush=True)
+        del buf
 Path("gpurun_out").mkdir(exist_ok=True)
 Path("gpurun_out/sparse_wide_bench.json").write_text(json.dumps(out, indent=1))
