@@ -149,6 +149,34 @@ int emul_pair_scores_wide(const uint8_t *a, int la, const uint8_t *b0, int lb0, 
     return 0;
 }
 
+// Words of up to 64 symbols under a dense similarity table: the block-wise path with the table-driven cell
+// (nwap_dp_blocks_tab; rows carry the table row offset a * K).
+int emul_pair_scores_wide_tab(const uint8_t *a, int la, const uint8_t *b0, int lb0, const uint8_t *b1, int lb1,
+                              const int8_t *sim, int K, int gap, int *s0, int *s1)
+{
+    if (la < 1 || la > NWAP_MAXLEN_WIDE || lb0 < 1 || lb1 < 1 || lb0 > NWAP_MAXLEN_WIDE || lb1 > NWAP_MAXLEN_WIDE || K > 128) return -1;
+    static uint8_t etab[128 * 128];
+    int M = -128;
+    for (int i = 0; i < K * K; ++i) M = sim[i] > M ? sim[i] : M;
+    for (int i = 0; i < K * K; ++i) etab[i] = (uint8_t)(M - sim[i]);
+    nwap_scheme_consts sc = nwap_make_consts(M, M, gap, 3);
+    sc.symmul = (uint32_t)K;
+    nwap_sym2 row2[NWAP_MAXLEN_WIDE + 1];
+    for (int i = 0; i < la; ++i) {
+        row2[i].a2 = nwap_row_code(a[i], sc);
+        row2[i].d0 = NWAP_BIAS2 + (uint32_t)i * sc.u2;
+    }
+    uint8_t p0[NWAP_MAXLEN_WIDE + NWAP_WB] = {0}, p1[NWAP_MAXLEN_WIDE + NWAP_WB] = {0};
+    memcpy(p0, b0, lb0);
+    memcpy(p1, b1, lb1);
+    const int LB = lb0 > lb1 ? lb0 : lb1;
+    uint32_t save[NWAP_MAXLEN_WIDE + 1];
+    const uint32_t v = nwap_dp_blocks_tab(row2, la, p0, p1, (LB + NWAP_WB - 1) / NWAP_WB, lb0, lb1, sc, save, etab);
+    *s0 = nwap_unbias(v & 0xffffu, la, lb0, sc);
+    *s1 = nwap_unbias(v >> 16, la, lb1, sc);
+    return 0;
+}
+
 // Scores (a vs b0) and (a vs b1) with the packed recurrence at register width LB.
 int emul_pair_scores(int flavor, int LB, const uint8_t *a, int la, const uint8_t *b0, int lb0,
                      const uint8_t *b1, int lb1, int match, int mismatch, int gap,

@@ -30,6 +30,7 @@ def emul():
     L.emul_pair_scores_ov.argtypes = [i, p, i, p, i, p, i, p, i, i, i, i, p, p]
     L.emul_pair_scores_tab.argtypes = [i, p, i, p, i, p, i, p, i, i, p, p]
     L.emul_pair_scores_wide.argtypes = [p, i, p, i, p, i, i, i, i, p, p]
+    L.emul_pair_scores_wide_tab.argtypes = [p, i, p, i, p, i, p, i, i, p, p]
     L.emul_row_of.restype = i64
     L.emul_row_of.argtypes = [i64, i64]
     L.emul_col_of.restype = i64
@@ -173,6 +174,34 @@ def test_dense_table_rows_match_oracle(emul):
                                          sim.ctypes.data, K, g, ctypes.addressof(s0), ctypes.addressof(s1)) == 0
         sim32 = sim.astype(np.int32)
         assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim32, g), orc.c_nw_score(a, b1, sim32, g)), (K, g, LB)
+
+
+def test_dense_table_blockwise_recurrence_for_long_words(emul):
+    """Override schemes over words of up to 64 symbols: the block-wise path with the table-driven cell."""
+    rng = random.Random(77)
+    for it in range(2500):
+        q = rng.choice([17, 25, 32, 33, 40, 48, 49, 63, 64])
+        K = rng.choice([2, 5, 17, 40, 128])
+        while True:
+            g = rng.randint(-2, 1)
+            lo_s, hi_s = sorted((rng.randint(-2, 2), rng.randint(-2, 2)))
+            if min(0, 2 * q * g, q * lo_s) >= -128 and max(0, 2 * q * g, q * hi_s) <= 127:
+                break
+        sim = np.zeros((K, K), dtype=np.int8)
+        for a_ in range(K):
+            for b_ in range(a_, K):
+                sim[a_, b_] = sim[b_, a_] = rng.randint(lo_s, hi_s)
+        la, lb0, lb1 = rng.randint(1, q), rng.randint(1, q), rng.randint(1, q)
+        if it % 7 == 0:
+            la = lb0 = lb1 = q
+        a = np.array([rng.randrange(K) for _ in range(la)], dtype=np.uint8)
+        b0 = np.array([rng.randrange(K) for _ in range(lb0)], dtype=np.uint8)
+        b1 = np.array([rng.randrange(K) for _ in range(lb1)], dtype=np.uint8)
+        s0, s1 = ctypes.c_int(), ctypes.c_int()
+        assert emul.emul_pair_scores_wide_tab(a.ctypes.data, la, b0.ctypes.data, lb0, b1.ctypes.data, lb1,
+                                              sim.ctypes.data, K, g, ctypes.addressof(s0), ctypes.addressof(s1)) == 0
+        sim32 = sim.astype(np.int32)
+        assert (s0.value, s1.value) == (orc.c_nw_score(a, b0, sim32, g), orc.c_nw_score(a, b1, sim32, g)), (K, g, q)
 
 
 def test_small_floor_division_is_exact(emul):

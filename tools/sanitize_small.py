@@ -64,3 +64,23 @@ with NwapContext(ids2, lens2, nw.ScoringScheme(1, -1, -1)) as ctx:
     ctx.score_range(0, P2, out)
     assert np.array_equal(out.cpu().numpy(), ref2), "wide"
     print("wide ok")
+# override scheme over the same long-word vocabulary (wide build of the table-driven cell) and its sparse output
+ov2 = {(0, 1): 0, (2, 5): 1, (3, 4): 0, (0, 6): 1}
+sch2 = nw.ScoringScheme(1, -1, -1, overrides=ov2)
+sim2o = orc.similarity_matrix(1, -1, 30, ov2)
+ref2o, *_ = orc.c_score_range(ids2.astype(np.int32), lens2.astype(np.int32), sim2o, -1, n2, 0, P2, threads=4)
+with NwapContext(ids2, lens2, sch2) as ctx:
+    out = torch.empty(P2, dtype=torch.int8, device="cuda")
+    ctx.score_range(0, P2, out)
+    assert np.array_equal(out.cpu().numpy(), ref2o), "override wide"
+    deg = torch.zeros(n2, dtype=torch.int32, device="cuda")
+    idx, sc, st = ctx.score_range_compact(0, P2, threshold=1, capacity=P2, degree=deg)
+    keep = np.flatnonzero(ref2o >= 1)
+    assert np.array_equal(idx.cpu().numpy(), keep) and np.array_equal(sc.cpu().numpy(), ref2o[keep]), "override wide sparse"
+    print("override wide ok", idx.numel())
+with NwapContext(ids, lens, sch) as ctx:
+    deg = torch.zeros(n, dtype=torch.int32, device="cuda")
+    idx, sc, st = ctx.score_range_compact(5, P - 7, threshold=2, capacity=P, degree=deg)
+    keep = np.flatnonzero(refo[5:P - 7] >= 2) + 5
+    assert np.array_equal(idx.cpu().numpy(), keep) and np.array_equal(sc.cpu().numpy(), refo[keep]), "override sparse output"
+    print("override sparse ok", idx.numel())
