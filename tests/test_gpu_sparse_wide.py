@@ -158,10 +158,11 @@ def test_long40_golden_runs_on_the_packed_kernel(golden_cases):
             ctx.score_range(0, P, out, variant="packed")      # the 2-IMAD A/B build stays at 32 symbols
 
 
-@pytest.mark.parametrize("qmax,gap", [(33, -1), (48, -1), (64, -1), (40, 0), (63, 1)])
+@pytest.mark.parametrize("qmax,gap", [(25, -2), (28, -2), (32, -2), (33, -1), (48, -1), (64, -1), (40, 0), (63, 1)])
 def test_long_words_block_path_vs_oracle(qmax, gap):
     """Random vocabularies mixing short words with words of up to 64 symbols: all bytes + statistics vs the
-    oracle, sub-ranges with misaligned outputs, and the sparse output on the wide build."""
+    oracle, sub-ranges with misaligned outputs, and the sparse output on the wide build (which uniform schemes take
+    from a longest word of 25 symbols on)."""
     rng = np.random.default_rng(1000 + qmax)
     n = 6000
     lens = np.clip(np.rint(rng.normal(8.5, 2.8, size=n)), 1, 24).astype(np.uint8)
