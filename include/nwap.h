@@ -41,8 +41,9 @@ extern "C" {
 
 /* kernel variants selectable per call (nwap_score_range `variant`) */
 #define NWAP_VARIANT_AUTO    0  /* the packed DPX tile kernel: PACKED3 for a uniform scheme, PACKED_TAB for an override
-                                 * scheme; words of 33..64 symbols (gap -1, engine.py:83-90) run the wide build of either.
-                                 * Every scheme and store the uint8 word store and the preflight admit is served there. */
+                                 * scheme; words of 25/33..64 symbols (64: gap -1, engine.py:83-90) run the wide build of
+                                 * either.  Only a vocabulary with a word over 64 symbols -- which the preflight admits for
+                                 * gap 0 alone -- falls back to SIMPLE. */
 #define NWAP_VARIANT_SIMPLE  1  /* one thread per pair, int32 cells, K x K table: any scheme, any q <= 255; the independent
                                  * second implementation the packed kernel is cross-checked against */
 #define NWAP_VARIANT_PACKED  2  /* s16x2 DPX tile kernel, 2 DPX + 2 IMAD per packed cell */

@@ -300,3 +300,26 @@ def test_sparse_output_of_an_override_scheme(K, q, dense):
         idx, sc, _ = ctx.score_range_compact(s, e, threshold=thr, capacity=len(ridx), out=dense_out)
         assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
         assert np.array_equal(dense_out.cpu().numpy(), ref[s:e])
+
+
+@pytest.mark.parametrize("scheme,overrides", [((1, -1, 0), None), ((1, 0, 0), None), ((1, -1, 0), {(0, 1): 0, (2, 3): 1})])
+def test_words_over_64_symbols_fall_back_to_the_generic_kernel(scheme, overrides):
+    """With gap 0 the int8 preflight admits words of up to 127 symbols (engine.py:83-90: 2*q*gap drops out).  The
+    packed kernel stops at 64; `auto` then runs the generic one-thread-per-pair kernel -- same bytes as the oracle,
+    and the packed variants refuse with the reference-facing error."""
+    rng = np.random.default_rng(127)
+    n, qmax, K = 900, 127, 9
+    lens = np.clip(np.rint(rng.normal(8.5, 2.8, size=n)), 1, 24).astype(np.uint8)
+    lens[rng.choice(n, size=30, replace=False)] = rng.integers(65, qmax + 1, size=30)
+    lens[0] = qmax
+    ids = rng.integers(0, K, size=(n, qmax)).astype(np.uint8)
+    sch = nw.ScoringScheme(*scheme, overrides=overrides or {})
+    P = nw.num_edges(n)
+    ref, rsum, rmin, rmax = _oracle(ids, lens, sch, 0, P)
+    with NwapContext(ids, lens, sch) as ctx:
+        out = torch.empty(P, dtype=torch.int8, device="cuda")
+        st = ctx.score_range(0, P, out)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        assert st[:4] == (rsum, rmin, rmax, P)
+        with pytest.raises(ValueError):
+            ctx.score_range(0, P, out, variant="packed_tab" if overrides else "packed3")
