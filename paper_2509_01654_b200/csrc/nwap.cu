@@ -112,6 +112,7 @@ struct nwap_ctx {
     int sm_count = 0;
     int64_t n = 0;
     int qmax = 0;          // longest word
+    double long_share = 0; // share of the vocabulary's symbols that sit in words of more than NWAP_WIDE_FROM symbols
     int qpad = 0;          // stored row width (multiple of 16)
     int match = 0, mismatch = 0, gap = 0;
     int K = 0;             // similarity table size (max symbol + 1 unless overridden)
@@ -336,7 +337,11 @@ int enqueue_score(nwap_ctx *c, int64_t start, int64_t end, int8_t *out_dev, int 
     // Uniform schemes take the wide build from 25 symbols on: its 24-wide bodies keep the fast2 family and the few
     // longer chunks go block-wise, which beats the 32-wide instantiation (no fast2, spills) by 29 % on a natural
     // vocabulary with a 25..32-symbol tail (tools/q32_bench.py).  The table-driven cell keeps its 32-wide build (+5 %).
-    const bool wide = !ov && ((flavor == 1 && c->qmax > NWAP_WIDE_FROM) || (flavor == 3 && c->qmax > NWAP_MAXLEN_FAST));
+    // The exception: a vocabulary MADE of 25..32-symbol words (every chunk would go block-wise: 10.0 against 14.5 TCUPS
+    // at a fixed length of 28).  The two builds cross where ~45 % of the cells sit in long chunks; the share of the
+    // symbols that belong to long words estimates that.
+    const bool mostly_long = c->qmax <= NWAP_MAXLEN_FAST && c->long_share > 0.40;
+    const bool wide = !ov && ((flavor == 1 && c->qmax > NWAP_WIDE_FROM && !mostly_long) || (flavor == 3 && c->qmax > NWAP_MAXLEN_FAST));
     const int qclass = wide ? 1 : c->qmax <= 16 ? 0 : c->qmax <= 24 ? 1 : 2;
     const int family = tab ? (wide ? (sparse ? 10 : 9) : sparse ? 8 : 4)
                            : wide ? (sparse ? 7 : 5) : sparse ? 6 : ov ? 3 : flavor;
@@ -514,7 +519,12 @@ int nwap_create(nwap_ctx **ctx_out, int device, const uint8_t *ids, int64_t n, i
     c->h_lens.assign(lengths, lengths + n);
     c->h_lenprefix.resize(n + 1);
     c->h_lenprefix[0] = 0;
-    for (int64_t i = 0; i < n; ++i) c->h_lenprefix[i + 1] = c->h_lenprefix[i] + lengths[i];
+    int64_t long_syms = 0;                                      // symbols of the words the 24-wide bodies cannot hold
+    for (int64_t i = 0; i < n; ++i) {
+        c->h_lenprefix[i + 1] = c->h_lenprefix[i] + lengths[i];
+        if (lengths[i] > NWAP_WIDE_FROM) long_syms += lengths[i];
+    }
+    c->long_share = (double)long_syms / (double)std::max<int64_t>(1, c->h_lenprefix[n]);
     c->h_rowpref.assign(n + 1, 0);
     for (int64_t r = 0; r < n; ++r)
         c->h_rowpref[r + 1] = c->h_rowpref[r] + (int64_t)lengths[r] * (c->h_lenprefix[n] - c->h_lenprefix[r + 1]);
