@@ -323,3 +323,30 @@ def test_words_over_64_symbols_fall_back_to_the_generic_kernel(scheme, overrides
         assert st[:4] == (rsum, rmin, rmax, P)
         with pytest.raises(ValueError):
             ctx.score_range(0, P, out, variant="packed_tab" if overrides else "packed3")
+
+
+def test_vocabulary_made_of_long_words_keeps_the_32_wide_build():
+    """More than 40 % of the symbols in words of 25..32 symbols: `auto` keeps the 32-wide instantiation (every chunk
+    would go block-wise on the wide build).  Bytes, statistics and the sparse output against the oracle."""
+    rng = np.random.default_rng(3232)
+    n, qmax = 3000, 32
+    lens = rng.integers(18, qmax + 1, size=n).astype(np.uint8)
+    lens[0] = qmax
+    ids = rng.integers(0, 30, size=(n, qmax)).astype(np.uint8)
+    scheme = nw.ScoringScheme(1, -1, -2)
+    P = nw.num_edges(n)
+    ref, rsum, rmin, rmax = _oracle(ids, lens, scheme, 0, P)
+    with NwapContext(ids, lens, scheme) as ctx:
+        out = torch.empty(P, dtype=torch.int8, device="cuda")
+        for variant in ("auto", "packed3", "packed", "simple"):
+            out.fill_(0x55)
+            st = ctx.score_range(0, P, out, variant=variant)
+            assert np.array_equal(out.cpu().numpy(), ref), variant
+            assert st[:4] == (rsum, rmin, rmax, P)
+        thr = int(np.percentile(ref, 99.9))
+        ridx, rsc, rdeg = orc.np_compact(ref, 0, n, thr)
+        degree = torch.zeros(n, dtype=torch.int32, device="cuda")
+        idx, sc, st2 = ctx.score_range_compact(0, P, threshold=thr, capacity=len(ridx), degree=degree)
+        assert np.array_equal(idx.cpu().numpy(), ridx) and np.array_equal(sc.cpu().numpy(), rsc)
+        assert np.array_equal(degree.cpu().numpy().astype(np.int64), rdeg)
+        assert st2 == (rsum, rmin, rmax, P)
